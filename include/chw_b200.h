@@ -1,0 +1,130 @@
+/*
+ * chw_b200.h — C ABI of the B200-native batched CHW (dyadic-order WHT) library.
+ *
+ * The reference exposes only a C++20 header API (the proj/include/chw headers; no C
+ * ABI, no FFI, no plugin registry — SURVEY §8b).  This header is the boundary a
+ * foreign caller binds; include/chw_b200/chw.hpp re-exposes the reference's own
+ * C++ signatures on top of it (the drop-in), and INTEGRATION.md shows both.
+ *
+ * Every entry point below replaces one reference interface:
+ *
+ *   chw_b200_forward        <- chw::chw_forward_inplace<T>
+ *                              (proj/include/chw/transforms.hpp:126-143), batched:
+ *                              `batch` contiguous rows of n elements, the loop the
+ *                              reference leaves to its caller (chw_main.cpp:65).
+ *                              Device pointers, stream-ordered, asynchronous.
+ *   chw_b200_forward_host   <- the same call on HOST buffers, synchronous like the
+ *                              reference (copies in and out are pipelined).
+ *   chw_b200_parallel_execute <- chw::parallel_execute_inplace<T>
+ *                              (proj/include/chw/parallel.hpp:16-17,
+ *                              proj/src/parallel.cpp:84-97): same validation
+ *                              (workers >= 1), same bitwise result as the serial
+ *                              transform; runs the batched kernel with batch = 1.
+ *   chw_b200_op_tally       <- chw::OpTally accounting (op_tally.hpp:12-22,
+ *                              transforms.hpp:75-78) in closed form.
+ *   chw_b200_workspace_bytes<- the optional `scratch` span of transforms.hpp:126-137
+ *                              (caller-owned scratch, allocated when absent).
+ *
+ * Errors never cross this boundary as exceptions: each call returns a
+ * chw_status and leaves the reference's exception text (same wording as
+ * common.hpp:31-46, parallel.cpp:88-91) in a thread-local buffer,
+ * chw_b200_last_error().  The C++ shim turns them back into the reference's
+ * exception types.
+ *
+ * Thread safety: calls on different streams / disjoint buffers may run
+ * concurrently; there is no global mutable state visible to the
+ * caller besides the per-device workspace cache, which is internally locked.
+ */
+#ifndef CHW_B200_H
+#define CHW_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CHW_B200_ABI_VERSION 1
+
+typedef enum chw_status {
+  CHW_OK = 0,
+  CHW_ERR_LENGTH = 1,      /* length not a power of two (incl. 0)  -> std::invalid_argument */
+  CHW_ERR_MODE = 2,        /* Orthonormal on an integer signal       -> std::invalid_argument */
+  CHW_ERR_ARGUMENT = 3,    /* other bad argument (workers < 1, null) -> std::invalid_argument */
+  CHW_ERR_UNSUPPORTED = 4, /* dtype / size not supported by this build */
+  CHW_ERR_WORKSPACE = 5,   /* caller workspace too small */
+  CHW_ERR_CUDA = 6,        /* CUDA runtime error (text in last_error)  */
+  CHW_ERR_NO_DEVICE = 7,   /* no CUDA device visible                   */
+  CHW_ERR_RESOURCE = 8     /* allocation failed                 -> chw::ResourceError */
+} chw_status;
+
+/* Order matches chw::ScalingMode (proj/include/chw/common.hpp:15). */
+typedef enum chw_mode { CHW_ORTHONORMAL = 0, CHW_UNNORMALIZED = 1 } chw_mode;
+
+typedef enum chw_dtype {
+  CHW_F64 = 0,  /* reference `double` path; Orthonormal is bit-exact with the reference */
+  CHW_F32 = 1,  /* fp32 in/out, fp32 arithmetic, scale applied once at the end          */
+  CHW_BF16 = 2, /* bf16 in/out, fp32 arithmetic, one rounding at the output           */
+  CHW_I64 = 3   /* reference `std::int64_t` path: Unnormalized only, exact            */
+} chw_dtype;
+
+/* Output coefficient order.  DYADIC is the reference's
+ * chw_forward order; NATURAL = fwht_natural (transforms.hpp:147-172);
+ * SEQUENCY = dyadic_to_sequency applied to the dyadic output
+ * (orderings.hpp:82-90, apply_permutation :92-102). */
+typedef enum chw_order { CHW_ORDER_DYADIC = 0, CHW_ORDER_NATURAL = 1, CHW_ORDER_SEQUENCY = 2 } chw_order;
+
+/* Batched CHW transform, dyadic order.  `in` and `out` are device pointers to
+ * batch*n contiguous elements of `dtype` (in == out is allowed: in place).
+ * `workspace` may be NULL (the library allocates and caches one per device) or
+ * a device buffer of at least chw_b200_workspace_bytes(dtype, batch, n) bytes.
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Asynchronous. */
+chw_status chw_b200_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                            chw_mode mode, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Same, with an explicit output order (f2). */
+chw_status chw_b200_forward_ordered(const void* in, void* out, chw_dtype dtype, int64_t batch,
+                                    uint64_t n, chw_mode mode, chw_order order, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+
+/* Workspace the device call needs (0 for single-pass sizes). */
+size_t chw_b200_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
+
+/* Host-buffer call: copies `in_host` to the device, transforms, copies the
+ * result to `out_host` (may equal in_host), and returns when done — the
+ * reference's synchronous in-place contract.  Pinned host memory is used
+ * directly; pageable memory is staged through internal pinned buffers.
+ * Copies and kernels of consecutive row chunks overlap on two streams. */
+chw_status chw_b200_forward_host(const void* in_host, void* out_host, chw_dtype dtype,
+                                 int64_t batch, uint64_t n, chw_mode mode);
+
+/* parallel_execute_inplace(x, workers, mode) on a DEVICE buffer of one signal.
+ * Validation as parallel.cpp:84-91; the pool is replaced by the GPU. */
+chw_status chw_b200_parallel_execute(void* x, chw_dtype dtype, uint64_t n, int workers,
+                                     chw_mode mode, void* stream);
+
+/* Closed-form OpTally of one length-n transform:
+ *   op 0 = chw_forward  : adds m*2^m, mults m*2^m (Orthonormal) or 0
+ *   op 1 = haar_forward : adds 2(n-1), mults 2(n-1) (Orthonormal) or 0
+ *   op 2 = normalize    : adds 0, mults n
+ * n == 1 leaves both at 0. */
+chw_status chw_b200_op_tally(int op, uint64_t n, chw_mode mode, uint64_t* additions,
+                             uint64_t* multiplications);
+
+const char* chw_b200_status_string(chw_status s);
+const char* chw_b200_last_error(void);
+
+/* Number of kernels this library has launched in this process (all devices). */
+uint64_t chw_b200_launch_count(void);
+
+/* Name of the kernel family the dispatcher picks for (dtype, n): "k1-tuned",
+ * "k1-generic", "k4-multipass:<passes>", ... (for reports; never NULL). */
+const char* chw_b200_plan_name(chw_dtype dtype, uint64_t n);
+
+int chw_b200_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHW_B200_H */

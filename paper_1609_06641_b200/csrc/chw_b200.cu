@@ -1,0 +1,464 @@
+// chw_b200.cu — dispatch + C ABI (include/chw_b200.h).
+//
+// Host-side flow of chw_b200_forward (replaces chw::chw_forward_inplace,
+// transforms.hpp:126-143, applied to every row of a batch):
+//   validate (common.hpp:31-46 wording) -> pick the schedule for (dtype, m) ->
+//   launch K1 (one pass) or the K4 passes on the caller's stream.
+// No CPU fallback exists: without a device every call returns
+// CHW_ERR_NO_DEVICE / CHW_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/chw_b200.h"
+#include "launch.cuh"
+
+using namespace chwb;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+bool is_pow2(uint64_t n) { return n != 0 && (n & (n - 1)) == 0; }
+int level_of(uint64_t n) { return 63 - __builtin_clzll(n); }
+
+size_t elem_size(chw_dtype d) {
+  switch (d) {
+    case CHW_F64:
+    case CHW_I64:
+      return 8;
+    case CHW_F32:
+      return 4;
+    case CHW_BF16:
+      return 2;
+  }
+  return 0;
+}
+size_t inter_size(chw_dtype d) { return d == CHW_BF16 ? 4 : elem_size(d); }
+
+}  // namespace
+
+namespace chwb {
+chw_status fail(chw_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+chw_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? CHW_ERR_NO_DEVICE
+                                                                          : CHW_ERR_CUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+chw_status current_device(int* dev) {
+  CHW_CUDA(cudaGetDevice(dev));
+  if (*dev < 0 || *dev >= 64) return fail(CHW_ERR_UNSUPPORTED, "device index out of range");
+  return CHW_OK;
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace chwb
+
+namespace {
+
+// Reference validation order and text: require_pow2 then require_mode
+// (transforms.hpp:127-130, common.hpp:31-46).
+chw_status validate(const char* what, chw_dtype dtype, uint64_t n, chw_mode mode) {
+  if (!is_pow2(n))
+    return fail(CHW_ERR_LENGTH,
+                std::string(what) + ": length " + std::to_string(n) + " is not a power of two");
+  if (dtype == CHW_I64 && mode == CHW_ORTHONORMAL)
+    return fail(CHW_ERR_MODE,
+                std::string(what) + ": orthonormal mode requires a floating-point signal");
+  if (dtype != CHW_F64 && dtype != CHW_F32 && dtype != CHW_BF16 && dtype != CHW_I64)
+    return fail(CHW_ERR_UNSUPPORTED, std::string(what) + ": unknown dtype");
+  if (mode != CHW_ORTHONORMAL && mode != CHW_UNNORMALIZED)
+    return fail(CHW_ERR_ARGUMENT, std::string(what) + ": unknown scaling mode");
+  if (level_of(n) > kMaxM)
+    return fail(CHW_ERR_UNSUPPORTED, std::string(what) + ": length " + std::to_string(n) +
+                                         " exceeds the supported maximum 2^" + std::to_string(kMaxM));
+  return CHW_OK;
+}
+
+// 2^(-m/2): exact power of two for even m, one rounding of (2^-(m-1)/2)/sqrt2
+// for odd m (the product of the reference's m per-butterfly kInvSqrt2 factors).
+double ortho_scale(int m) {
+  double s = std::ldexp(1.0, -(m / 2));
+  if (m & 1) s *= 0.70710678118654752440;
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// Per-device state: SM count, lazily-grown workspace, streams for the host path.
+// ---------------------------------------------------------------------------
+struct DeviceState {
+  std::mutex mu;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  int sms = 0;
+  // host path
+  cudaStream_t streams[2] = {nullptr, nullptr};
+  void* dbuf[2] = {nullptr, nullptr};
+  size_t dbuf_bytes = 0;
+  void* pinned[2] = {nullptr, nullptr};
+  size_t pinned_bytes = 0;
+  cudaEvent_t done[2] = {nullptr, nullptr};
+};
+DeviceState g_dev[64];
+
+chw_status ensure_workspace(int dev, size_t bytes, void** out) {
+  DeviceState& s = g_dev[dev];
+  std::lock_guard<std::mutex> lk(s.mu);
+  if (s.ws_bytes < bytes) {
+    if (s.ws) {
+      cudaDeviceSynchronize();  // the old workspace may still be in use by queued work
+      cudaFree(s.ws);
+      s.ws = nullptr;
+      s.ws_bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&s.ws, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(CHW_ERR_RESOURCE, "chw_forward: cannot allocate " + std::to_string(bytes) +
+                                        " bytes of workspace: " + cudaGetErrorString(e));
+    }
+    s.ws_bytes = bytes;
+  }
+  *out = s.ws;
+  return CHW_OK;
+}
+
+size_t workspace_for(chw_dtype dtype, int64_t batch, int m) {
+  int k1max = 0;
+  switch (dtype) {
+    case CHW_F64:
+      k1max = Regime<double>::K1MAX;
+      break;
+    case CHW_I64:
+      k1max = Regime<long long>::K1MAX;
+      break;
+    case CHW_F32:
+      k1max = Regime<float>::K1MAX;
+      break;
+    case CHW_BF16:
+      k1max = Regime<__nv_bfloat16>::K1MAX;
+      break;
+  }
+  if (m <= k1max || batch <= 0) return 0;
+  return (size_t)batch * ((size_t)1 << m) * inter_size(dtype);
+}
+
+chw_status forward_impl(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                        chw_mode mode, chw_order order, void* workspace, size_t workspace_bytes,
+                        cudaStream_t st) {
+  if (chw_status s = validate("chw_forward", dtype, n, mode)) return s;
+  if (batch < 0) return fail(CHW_ERR_ARGUMENT, "chw_forward: negative batch");
+  if (order != CHW_ORDER_DYADIC)
+    return fail(CHW_ERR_UNSUPPORTED, "chw_forward: only dyadic order is built in this version");
+  if (batch == 0) return CHW_OK;
+  if (!in || !out) return fail(CHW_ERR_ARGUMENT, "chw_forward: null buffer");
+  const int m = level_of(n);
+  const size_t need = workspace_for(dtype, batch, m);
+  void* ws = workspace;
+  if (need > 0) {
+    if (ws == nullptr) {
+      int dev = 0;
+      if (chw_status s = current_device(&dev)) return s;
+      if (chw_status s = ensure_workspace(dev, need, &ws)) return s;
+    } else if (workspace_bytes < need) {
+      return fail(CHW_ERR_WORKSPACE, "chw_forward: workspace of " + std::to_string(workspace_bytes) +
+                                         " bytes is smaller than the " + std::to_string(need) +
+                                         " required");
+    }
+  }
+  const bool ortho = (mode == CHW_ORTHONORMAL);
+  switch (dtype) {
+    case CHW_F64: {
+      auto* i = static_cast<const double*>(in);
+      auto* o = static_cast<double*>(out);
+      return m <= Regime<double>::K1MAX ? forward_k1<double>(m, ortho, i, o, batch, 1.0, st)
+                                        : forward_k4<double>(m, ortho, i, o, ws, batch, 1.0, st);
+    }
+    case CHW_I64: {
+      auto* i = static_cast<const long long*>(in);
+      auto* o = static_cast<long long*>(out);
+      return m <= Regime<long long>::K1MAX
+                 ? forward_k1<long long>(m, false, i, o, batch, 1, st)
+                 : forward_k4<long long>(m, false, i, o, ws, batch, 1, st);
+    }
+    case CHW_F32: {
+      auto* i = static_cast<const float*>(in);
+      auto* o = static_cast<float*>(out);
+      const float sc = (float)ortho_scale(m);
+      return m <= Regime<float>::K1MAX ? forward_k1<float>(m, ortho, i, o, batch, sc, st)
+                                       : forward_k4<float>(m, ortho, i, o, ws, batch, sc, st);
+    }
+    case CHW_BF16: {
+      auto* i = static_cast<const __nv_bfloat16*>(in);
+      auto* o = static_cast<__nv_bfloat16*>(out);
+      const float sc = (float)ortho_scale(m);
+      return m <= Regime<__nv_bfloat16>::K1MAX
+                 ? forward_k1<__nv_bfloat16>(m, ortho, i, o, batch, sc, st)
+                 : forward_k4<__nv_bfloat16>(m, ortho, i, o, ws, batch, sc, st);
+    }
+  }
+  return fail(CHW_ERR_UNSUPPORTED, "chw_forward: unknown dtype");
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer path: rows are processed in chunks; chunk c uses stream c%2, so
+// the H2D copy of chunk c+1, the kernels of chunk c and the D2H copy of chunk
+// c-1 overlap (two copy engines + compute).
+// ---------------------------------------------------------------------------
+chw_status host_impl(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
+                     uint64_t n, chw_mode mode) {
+  if (chw_status s = validate("chw_forward", dtype, n, mode)) return s;
+  if (batch < 0) return fail(CHW_ERR_ARGUMENT, "chw_forward: negative batch");
+  if (batch == 0) return CHW_OK;
+  if (!in_host || !out_host) return fail(CHW_ERR_ARGUMENT, "chw_forward: null buffer");
+  int dev = 0;
+  if (chw_status s = current_device(&dev)) return s;
+  DeviceState& d = g_dev[dev];
+  std::lock_guard<std::mutex> lk(d.mu);
+
+  const size_t es = elem_size(dtype);
+  const size_t row_bytes = (size_t)n * es;
+  const int m = level_of(n);
+  // ~64 MiB chunks (at least one row).
+  const size_t target = (size_t)64 << 20;
+  int64_t rows_per_chunk = (int64_t)std::max<size_t>(1, target / row_bytes);
+  rows_per_chunk = std::min<int64_t>(rows_per_chunk, batch);
+  const size_t chunk_bytes = (size_t)rows_per_chunk * row_bytes;
+
+  for (int i = 0; i < 2; ++i)
+    if (!d.streams[i]) {
+      CHW_CUDA(cudaStreamCreateWithFlags(&d.streams[i], cudaStreamNonBlocking));
+      CHW_CUDA(cudaEventCreateWithFlags(&d.done[i], cudaEventDisableTiming));
+    }
+  if (d.dbuf_bytes < chunk_bytes) {
+    for (int i = 0; i < 2; ++i) {
+      if (d.dbuf[i]) cudaFree(d.dbuf[i]);
+      d.dbuf[i] = nullptr;
+    }
+    d.dbuf_bytes = 0;
+    for (int i = 0; i < 2; ++i)
+      if (cudaMalloc(&d.dbuf[i], chunk_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CHW_ERR_RESOURCE, "chw_forward: cannot allocate device staging buffers");
+      }
+    d.dbuf_bytes = chunk_bytes;
+  }
+  // Workspace for multi-pass sizes, one per stream.
+  const size_t ws_chunk = workspace_for(dtype, rows_per_chunk, m);
+  std::vector<void*> wss(2, nullptr);
+  void* ws_all = nullptr;
+  if (ws_chunk > 0) {
+    DeviceState& s = d;
+    if (s.ws_bytes < 2 * ws_chunk) {
+      if (s.ws) {
+        cudaDeviceSynchronize();
+        cudaFree(s.ws);
+      }
+      s.ws = nullptr;
+      s.ws_bytes = 0;
+      if (cudaMalloc(&s.ws, 2 * ws_chunk) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CHW_ERR_RESOURCE, "chw_forward: cannot allocate workspace");
+      }
+      s.ws_bytes = 2 * ws_chunk;
+    }
+    ws_all = s.ws;
+    wss[0] = ws_all;
+    wss[1] = static_cast<char*>(ws_all) + ws_chunk;
+  }
+
+  cudaPointerAttributes ai{}, ao{};
+  const bool in_pinned = cudaPointerGetAttributes(&ai, in_host) == cudaSuccess &&
+                         ai.type == cudaMemoryTypeHost;
+  const bool out_pinned = cudaPointerGetAttributes(&ao, out_host) == cudaSuccess &&
+                          ao.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  const bool staged = !(in_pinned && out_pinned);
+  if (staged && d.pinned_bytes < chunk_bytes) {
+    for (int i = 0; i < 2; ++i) {
+      if (d.pinned[i]) cudaFreeHost(d.pinned[i]);
+      d.pinned[i] = nullptr;
+    }
+    d.pinned_bytes = 0;
+    for (int i = 0; i < 2; ++i)
+      if (cudaMallocHost(&d.pinned[i], chunk_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(CHW_ERR_RESOURCE, "chw_forward: cannot allocate pinned staging buffers");
+      }
+    d.pinned_bytes = chunk_bytes;
+  }
+
+  const char* src = static_cast<const char*>(in_host);
+  char* dst = static_cast<char*>(out_host);
+  const int64_t nchunks = (batch + rows_per_chunk - 1) / rows_per_chunk;
+  // In the staged path chunk c's output must land in out_host before the
+  // pinned buffer is reused for chunk c+2; the event wait below orders that.
+  std::vector<int64_t> pending_rows(2, 0), pending_row0(2, 0);
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int b = (int)(c & 1);
+    cudaStream_t st = d.streams[b];
+    const int64_t r0 = c * rows_per_chunk;
+    const int64_t rows = std::min<int64_t>(rows_per_chunk, batch - r0);
+    const size_t bytes = (size_t)rows * row_bytes;
+    if (staged) {
+      // Drain the previous use of this buffer pair (chunk c-2).
+      CHW_CUDA(cudaEventSynchronize(d.done[b]));
+      if (pending_rows[b] > 0) {
+        if (!out_pinned)
+          std::memcpy(dst + (size_t)pending_row0[b] * row_bytes, d.pinned[b],
+                      (size_t)pending_rows[b] * row_bytes);
+        pending_rows[b] = 0;
+      }
+      const void* h_in = src + (size_t)r0 * row_bytes;
+      if (!in_pinned) {
+        std::memcpy(d.pinned[b], h_in, bytes);
+        h_in = d.pinned[b];
+      }
+      CHW_CUDA(cudaMemcpyAsync(d.dbuf[b], h_in, bytes, cudaMemcpyHostToDevice, st));
+    } else {
+      CHW_CUDA(cudaMemcpyAsync(d.dbuf[b], src + (size_t)r0 * row_bytes, bytes,
+                               cudaMemcpyHostToDevice, st));
+    }
+    if (chw_status s = forward_impl(d.dbuf[b], d.dbuf[b], dtype, rows, n, mode, CHW_ORDER_DYADIC,
+                                    wss[b], ws_chunk, st))
+      return s;
+    void* h_out = (staged && !out_pinned) ? d.pinned[b] : dst + (size_t)r0 * row_bytes;
+    CHW_CUDA(cudaMemcpyAsync(h_out, d.dbuf[b], bytes, cudaMemcpyDeviceToHost, st));
+    CHW_CUDA(cudaEventRecord(d.done[b], st));
+    if (staged && !out_pinned) {
+      pending_rows[b] = rows;
+      pending_row0[b] = r0;
+    }
+  }
+  for (int b = 0; b < 2; ++b) {
+    CHW_CUDA(cudaEventSynchronize(d.done[b]));
+    if (pending_rows[b] > 0)
+      std::memcpy(dst + (size_t)pending_row0[b] * row_bytes, d.pinned[b],
+                  (size_t)pending_rows[b] * row_bytes);
+  }
+  (void)ws_all;
+  return CHW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+chw_status chw_b200_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                            chw_mode mode, void* workspace, size_t workspace_bytes, void* stream) {
+  return forward_impl(in, out, dtype, batch, n, mode, CHW_ORDER_DYADIC, workspace, workspace_bytes,
+                      static_cast<cudaStream_t>(stream));
+}
+
+chw_status chw_b200_forward_ordered(const void* in, void* out, chw_dtype dtype, int64_t batch,
+                                    uint64_t n, chw_mode mode, chw_order order, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  return forward_impl(in, out, dtype, batch, n, mode, order, workspace, workspace_bytes,
+                      static_cast<cudaStream_t>(stream));
+}
+
+size_t chw_b200_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {
+  if (!is_pow2(n)) return 0;
+  return workspace_for(dtype, batch, level_of(n));
+}
+
+chw_status chw_b200_forward_host(const void* in_host, void* out_host, chw_dtype dtype,
+                                 int64_t batch, uint64_t n, chw_mode mode) {
+  return host_impl(in_host, out_host, dtype, batch, n, mode);
+}
+
+chw_status chw_b200_parallel_execute(void* x, chw_dtype dtype, uint64_t n, int workers,
+                                     chw_mode mode, void* stream) {
+  // parallel.cpp:84-91: require_pow2, require_mode, then workers >= 1.
+  if (chw_status s = validate("parallel_execute", dtype, n, mode)) return s;
+  if (workers < 1)
+    return fail(CHW_ERR_ARGUMENT,
+                "parallel_execute: workers must be >= 1, got " + std::to_string(workers));
+  return forward_impl(x, x, dtype, 1, n, mode, CHW_ORDER_DYADIC, nullptr, 0,
+                      static_cast<cudaStream_t>(stream));
+}
+
+chw_status chw_b200_op_tally(int op, uint64_t n, chw_mode mode, uint64_t* additions,
+                             uint64_t* multiplications) {
+  if (!is_pow2(n)) return fail(CHW_ERR_LENGTH, "op_tally: length " + std::to_string(n) +
+                                                   " is not a power of two");
+  const uint64_t m = (uint64_t)level_of(n);
+  uint64_t a = 0, mu = 0;
+  const bool ortho = (mode == CHW_ORTHONORMAL);
+  switch (op) {
+    case 0:  // chw_forward: m levels of n adds (transforms.hpp:75-78)
+      a = m * n;
+      mu = ortho ? m * n : 0;
+      break;
+    case 1:  // haar_forward: sum_{len=n..2} len = 2(n-1)
+      a = 2 * (n - 1);
+      mu = ortho ? 2 * (n - 1) : 0;
+      break;
+    case 2:  // normalize: n multiplications (transforms.hpp:209)
+      mu = n;
+      break;
+    default:
+      return fail(CHW_ERR_ARGUMENT, "op_tally: unknown op");
+  }
+  if (additions) *additions = a;
+  if (multiplications) *multiplications = mu;
+  return CHW_OK;
+}
+
+const char* chw_b200_status_string(chw_status s) {
+  switch (s) {
+    case CHW_OK:
+      return "ok";
+    case CHW_ERR_LENGTH:
+      return "length is not a power of two";
+    case CHW_ERR_MODE:
+      return "orthonormal mode requires a floating-point signal";
+    case CHW_ERR_ARGUMENT:
+      return "invalid argument";
+    case CHW_ERR_UNSUPPORTED:
+      return "unsupported";
+    case CHW_ERR_WORKSPACE:
+      return "workspace too small";
+    case CHW_ERR_CUDA:
+      return "CUDA error";
+    case CHW_ERR_NO_DEVICE:
+      return "no CUDA device";
+    case CHW_ERR_RESOURCE:
+      return "resource allocation failed";
+  }
+  return "unknown status";
+}
+
+const char* chw_b200_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t chw_b200_launch_count(void) { return g_launches.load(); }
+
+const char* chw_b200_plan_name(chw_dtype dtype, uint64_t n) {
+  if (!is_pow2(n)) return "invalid";
+  const int m = level_of(n);
+  switch (dtype) {
+    case CHW_F64:
+      return plan_name<double>(m);
+    case CHW_I64:
+      return plan_name<long long>(m);
+    case CHW_F32:
+      return plan_name<float>(m);
+    case CHW_BF16:
+      return plan_name<__nv_bfloat16>(m);
+  }
+  return "invalid";
+}
+
+int chw_b200_abi_version(void) { return CHW_B200_ABI_VERSION; }
+
+}  // extern "C"

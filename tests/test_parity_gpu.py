@@ -1,0 +1,291 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the oracle.
+
+Bars (BASELINE.json north_star): f64 BIT-EXACT with the reference (stricter
+than the 1e-12 relative-L2 bar), int64 exact, fp32 relative
+L2 <= 1e-5, bf16 relative L2 <= 1e-2, and the dyadic output order checked
+bit-exactly through the Unnormalized integer probe (a wrong permutation cannot
+pass).  Inputs are seeded; sizes are ones the oracle finishes in seconds.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+O, U = oracle.ORTHONORMAL, oracle.UNNORMALIZED
+F32_TOL = 1e-5
+BF16_TOL = 1e-2
+
+
+def _chw():
+    import paper_1609_06641_b200 as chw
+
+    return chw
+
+
+def _gpu(x, cuda):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).to(cuda)
+
+
+def _run(x, mode, cuda, dtype=None):
+    import torch
+
+    chw = _chw()
+    t = _gpu(x, cuda)
+    if dtype is not None:
+        t = t.to(dtype)
+    chw.chw_forward_batched_(t, chw.ScalingMode(mode))
+    torch.cuda.synchronize()
+    return t
+
+
+def _rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def _rows_for(m, elems=1 << 16):
+    return max(1, min(37, elems >> m))
+
+
+# ---------------------------------------------------------------------------
+# f64: bit-exact against the reference algorithm (Orthonormal and Unnormalized)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m", list(range(0, 21)))
+@pytest.mark.parametrize("mode", [O, U])
+def test_f64_bitexact(cuda, m, mode):
+    rng = np.random.default_rng(100 + m)
+    rows = _rows_for(m) if m < 17 else 1
+    x = rng.uniform(-1, 1, size=(rows, 1 << m))
+    y = _run(x, mode, cuda).cpu().numpy()
+    ref = oracle.chw_batch(x, mode)
+    assert np.array_equal(y.view(np.uint64), ref.view(np.uint64)), (
+        f"m={m} mode={mode}: max abs diff {np.max(np.abs(y - ref))}")
+
+
+def test_f64_golden_cfg1_rows(cuda, golden):
+    x = golden["cfg1_rows16_in"].reshape(16, 1024)
+    y = _run(x, O, cuda).cpu().numpy()
+    assert np.array_equal(y.view(np.uint64), golden["cfg1_rows16_out"].reshape(16, 1024).view(np.uint64))
+
+
+@pytest.mark.parametrize("m", range(0, 15))
+def test_f64_golden_sweep(cuda, golden, m):
+    x = golden[f"sweep_f64_m{m}_in"][None, :]
+    for mode, key in ((O, "ortho"), (U, "unnorm")):
+        y = _run(x, mode, cuda).cpu().numpy()[0]
+        assert np.array_equal(y.view(np.uint64), golden[f"sweep_f64_m{m}_{key}"].view(np.uint64))
+
+
+# ---------------------------------------------------------------------------
+# int64 (f1): exact
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m", list(range(0, 21)))
+def test_i64_exact(cuda, m):
+    rng = np.random.default_rng(200 + m)
+    rows = _rows_for(m) if m < 17 else 1
+    x = rng.integers(-1000, 1001, size=(rows, 1 << m), dtype=np.int64)
+    y = _run(x, U, cuda).cpu().numpy()
+    assert np.array_equal(y, oracle.chw_batch(x, U))
+
+
+@pytest.mark.parametrize("m", range(0, 9))
+def test_i64_golden_dense(cuda, golden, m):
+    # transforms_test.cpp:123-132 through the GPU
+    x = golden[f"dense_int_m{m}_in"].reshape(20, 1 << m)
+    y = _run(x, U, cuda).cpu().numpy()
+    assert np.array_equal(y, golden[f"dense_int_m{m}_dense"].reshape(20, 1 << m))
+
+
+def test_i64_orthonormal_rejected(cuda):
+    chw = _chw()
+    import torch
+
+    t = torch.zeros(4, dtype=torch.int64, device=cuda)
+    with pytest.raises(ValueError, match="orthonormal mode requires a floating-point signal"):
+        chw.chw_forward_batched_(t, chw.ScalingMode.Orthonormal)
+
+
+# ---------------------------------------------------------------------------
+# fp32: tolerance + exact order probe
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m", list(range(0, 25)))
+def test_f32_tolerance(cuda, m):
+    import torch
+
+    rng = np.random.default_rng(300 + m)
+    rows = _rows_for(m, 1 << 18) if m < 20 else 1
+    x = rng.standard_normal(size=(rows, 1 << m)).astype(np.float32)
+    y = _run(x, O, cuda, torch.float32).cpu().numpy()
+    ref = oracle.chw_batch(x.astype(np.float64), O)
+    per_row = [_rel_l2(y[r], ref[r]) for r in range(rows)]
+    assert max(per_row) <= F32_TOL, f"m={m}: worst row rel L2 {max(per_row):.3e}"
+
+
+@pytest.mark.parametrize("m", list(range(0, 25)))
+def test_f32_order_probe_exact(cuda, m):
+    """Unnormalized on integers with |x| <= 2^(24-m): every partial sum is exact
+    in fp32, so the output must equal the int64 oracle bit for bit."""
+    import torch
+
+    rng = np.random.default_rng(400 + m)
+    bound = max(1, 1 << max(0, 24 - m - 1))
+    rows = _rows_for(m, 1 << 18) if m < 20 else 1
+    xi = rng.integers(-bound, bound + 1, size=(rows, 1 << m), dtype=np.int64)
+    y = _run(xi.astype(np.float32), U, cuda, torch.float32).cpu().numpy()
+    ref = oracle.chw_batch(xi, U)
+    assert np.array_equal(y.astype(np.int64), ref)
+    assert np.array_equal(y, ref.astype(np.float32))
+
+
+def test_f32_basis_vectors(cuda):
+    """e_j -> column j of H_dy: y[i] = 2^(-m/2) (-1)^popcount(rev(i) & j)."""
+    import torch
+
+    m = 12
+    n = 1 << m
+    js = [0, 1, 2, 3, 5, 100, 2047, 4095]
+    x = np.zeros((len(js), n), np.float32)
+    for r, j in enumerate(js):
+        x[r, j] = 1
+    y = _run(x, O, cuda, torch.float32).cpu().numpy()
+    rev = np.array([oracle.bit_reverse(i, m) for i in range(n)])
+    for r, j in enumerate(js):
+        sign = 1 - 2 * (np.array([bin(int(v) & j).count("1") & 1 for v in rev]))
+        assert np.array_equal(y[r], (sign * 2.0 ** (-m / 2)).astype(np.float32))
+
+
+# ---------------------------------------------------------------------------
+# bf16
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m", list(range(0, 21)))
+def test_bf16_tolerance(cuda, m):
+    import torch
+
+    rng = np.random.default_rng(500 + m)
+    rows = _rows_for(m, 1 << 18) if m < 18 else 1
+    x = torch.from_numpy(rng.standard_normal(size=(rows, 1 << m)).astype(np.float32)).to(torch.bfloat16)
+    xd = x.to(torch.float64).numpy()  # exact upcast of the same bf16 bytes
+    y = _run(x.numpy() if False else x.to(torch.float32).numpy(), O, cuda, torch.bfloat16)
+    y = y.to(torch.float64).cpu().numpy()
+    ref = oracle.chw_batch(xd, O)
+    per_row = [_rel_l2(y[r], ref[r]) for r in range(rows)]
+    assert max(per_row) <= BF16_TOL, f"m={m}: worst row rel L2 {max(per_row):.3e}"
+
+
+@pytest.mark.parametrize("m", list(range(0, 8)))
+def test_bf16_order_probe_exact(cuda, m):
+    """x in {-1,0,1}, m <= 7: |y| <= 128, exact in bf16."""
+    import torch
+
+    rng = np.random.default_rng(600 + m)
+    rows = 4099
+    xi = rng.integers(-1, 2, size=(rows, 1 << m), dtype=np.int64)
+    y = _run(xi.astype(np.float32), U, cuda, torch.bfloat16).to(torch.float64).cpu().numpy()
+    assert np.array_equal(y.astype(np.int64), oracle.chw_batch(xi, U))
+
+
+# ---------------------------------------------------------------------------
+# API behaviour: in place vs out of place, host path, parallel_execute, errors
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m", [3, 10, 12, 16])
+def test_out_of_place_equals_in_place(cuda, m):
+    import torch
+
+    chw = _chw()
+    rng = np.random.default_rng(700 + m)
+    x = _gpu(rng.uniform(-1, 1, size=(5, 1 << m)), cuda)
+    out = torch.empty_like(x)
+    chw.chw_forward_batched_(x, chw.ScalingMode.Orthonormal, out=out)
+    inplace = x.clone()
+    chw.chw_forward_batched_(inplace, chw.ScalingMode.Orthonormal)
+    torch.cuda.synchronize()
+    assert torch.equal(out, inplace)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32", "i64"])
+@pytest.mark.parametrize("m", [0, 7, 12, 16])
+def test_host_path(cuda, dtype, m):
+    chw = _chw()
+    rng = np.random.default_rng(800 + m)
+    rows = 9
+    if dtype == "i64":
+        x = rng.integers(-1000, 1001, size=(rows, 1 << m), dtype=np.int64)
+        mode = U
+    else:
+        x = rng.uniform(-1, 1, size=(rows, 1 << m)).astype(np.float64 if dtype == "f64" else np.float32)
+        mode = O
+    y = x.copy()
+    chw.chw_forward_host_(y, chw.ScalingMode(mode))
+    dev = _run(x, mode, cuda).cpu().numpy()
+    assert np.array_equal(y, dev)
+
+
+def test_kats_through_reference_api(cuda):
+    chw = _chw()
+    import torch
+
+    t = chw.OpTally()
+    y = chw.chw_forward(np.array([1, 0, 0, 0], np.int64), chw.ScalingMode.Unnormalized, t)
+    assert y.tolist() == [1, 1, 1, 1] and t.additions == 8
+    assert chw.chw_forward(np.array([0, 1, 0, 0], np.int64), chw.ScalingMode.Unnormalized).tolist() == [1, 1, -1, -1]
+    t.reset()
+    assert chw.chw_forward(np.array([9], np.int64), chw.ScalingMode.Unnormalized, t).tolist() == [9]
+    assert t == chw.OpTally()
+    with pytest.raises(ValueError, match="length 3 is not a power of two"):
+        chw.chw_forward_inplace(torch.zeros(3, dtype=torch.int64, device=cuda), chw.ScalingMode.Unnormalized)
+    with pytest.raises(ValueError, match="length 0 is not a power of two"):
+        chw.chw_forward_inplace(torch.zeros(0, dtype=torch.int64, device=cuda), chw.ScalingMode.Unnormalized)
+
+
+def test_parallel_execute_contract(cuda):
+    # parallel_test.cpp:21-91 restated
+    chw = _chw()
+    import torch
+
+    rng = np.random.default_rng(9)
+    for m in (2, 5, 9, 13):
+        x = rng.integers(-1000, 1001, size=1 << m, dtype=np.int64)
+        serial = oracle.chw_forward(x, U)
+        for workers in (1, 2, 4, 8):
+            t = chw.OpTally()
+            y = chw.parallel_execute(torch.from_numpy(x).to(cuda), workers, chw.ScalingMode.Unnormalized, t)
+            assert np.array_equal(y.cpu().numpy(), serial)
+            assert t.additions == m << m and t.multiplications == 0
+    for m in (3, 8, 11):
+        x = rng.uniform(-1, 1, size=1 << m)
+        serial = oracle.chw_forward(x, O)
+        y = chw.parallel_execute(torch.from_numpy(x).to(cuda), 4, chw.ScalingMode.Orthonormal).cpu().numpy()
+        assert np.array_equal(y.view(np.uint64), serial.view(np.uint64))
+    assert chw.parallel_execute(torch.tensor([1, 2], device=cuda), 8, chw.ScalingMode.Unnormalized).tolist() == [3, -1]
+    with pytest.raises(ValueError, match="workers must be >= 1, got 0"):
+        chw.parallel_execute(torch.tensor([1, 2, 3, 4], device=cuda), 0, chw.ScalingMode.Unnormalized)
+    with pytest.raises(ValueError, match="not a power of two"):
+        chw.parallel_execute(torch.tensor([1, 2, 3], device=cuda), 2, chw.ScalingMode.Unnormalized)
+    with pytest.raises(ValueError, match="orthonormal mode requires"):
+        chw.parallel_execute(torch.tensor([1, 2, 3, 4], device=cuda), 2, chw.ScalingMode.Orthonormal)
+
+
+def test_determinism(cuda):
+    # parallel_test.cpp:60-65 analogue: repeated runs are bitwise identical.
+    import torch
+
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal(size=(64, 1 << 16)).astype(np.float32)
+    first = _run(x, O, cuda, torch.float32)
+    for _ in range(5):
+        assert torch.equal(_run(x, O, cuda, torch.float32), first)
+
+
+def test_launches_counted(cuda):
+    chw = _chw()
+    import torch
+
+    before = chw.launch_count()
+    _run(np.zeros((4, 1 << 12), np.float32), O, cuda, torch.float32)
+    assert chw.launch_count() > before
