@@ -124,6 +124,14 @@ const char* chw_b200_plan_name(chw_dtype dtype, uint64_t n);
 
 int chw_b200_abi_version(void);
 
+/* 1 if `p` is device (or managed) memory of the current CUDA context, 0 for
+ * host memory (pinned or pageable).  Lets the C++ shim route spans without
+ * including CUDA headers. */
+int chw_b200_is_device_pointer(const void* p);
+
+/* cudaStreamSynchronize(stream) (NULL = legacy default stream). */
+chw_status chw_b200_stream_synchronize(void* stream);
+
 #ifdef __cplusplus
 }
 #endif

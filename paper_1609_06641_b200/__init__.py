@@ -59,6 +59,8 @@ EXPORTED_SYMBOLS = (
     "chw_b200_launch_count",
     "chw_b200_plan_name",
     "chw_b200_abi_version",
+    "chw_b200_is_device_pointer",
+    "chw_b200_stream_synchronize",
 )
 
 
@@ -134,6 +136,10 @@ def _load() -> ctypes.CDLL:
     lib.chw_b200_plan_name.restype = c.c_char_p
     lib.chw_b200_abi_version.argtypes = []
     lib.chw_b200_abi_version.restype = c.c_int
+    lib.chw_b200_is_device_pointer.argtypes = [c.c_void_p]
+    lib.chw_b200_is_device_pointer.restype = c.c_int
+    lib.chw_b200_stream_synchronize.argtypes = [c.c_void_p]
+    lib.chw_b200_stream_synchronize.restype = c.c_int
     return lib
 
 

@@ -461,4 +461,19 @@ const char* chw_b200_plan_name(chw_dtype dtype, uint64_t n) {
 
 int chw_b200_abi_version(void) { return CHW_B200_ABI_VERSION; }
 
+int chw_b200_is_device_pointer(const void* p) {
+  if (!p) return 0;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? 1 : 0;
+}
+
+chw_status chw_b200_stream_synchronize(void* stream) {
+  CHW_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return CHW_OK;
+}
+
 }  // extern "C"
