@@ -134,23 +134,18 @@ chw_status ensure_workspace(int dev, size_t bytes, void** out) {
 }
 
 size_t workspace_for(chw_dtype dtype, int64_t batch, int m) {
-  int k1max = 0;
+  if (batch <= 0) return 0;
   switch (dtype) {
     case CHW_F64:
-      k1max = Regime<double>::K1MAX;
-      break;
+      return m <= Regime<double>::K1MAX ? 0 : k4_workspace<double>(m, batch);
     case CHW_I64:
-      k1max = Regime<long long>::K1MAX;
-      break;
+      return m <= Regime<long long>::K1MAX ? 0 : k4_workspace<long long>(m, batch);
     case CHW_F32:
-      k1max = Regime<float>::K1MAX;
-      break;
+      return m <= Regime<float>::K1MAX ? 0 : k4_workspace<float>(m, batch);
     case CHW_BF16:
-      k1max = Regime<__nv_bfloat16>::K1MAX;
-      break;
+      return m <= Regime<__nv_bfloat16>::K1MAX ? 0 : k4_workspace<__nv_bfloat16>(m, batch);
   }
-  if (m <= k1max || batch <= 0) return 0;
-  return (size_t)batch * ((size_t)1 << m) * inter_size(dtype);
+  return 0;
 }
 
 chw_status forward_impl(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
@@ -254,7 +249,8 @@ chw_status host_impl(const void* in_host, void* out_host, chw_dtype dtype, int64
     d.dbuf_bytes = chunk_bytes;
   }
   // Workspace for multi-pass sizes, one per stream.
-  const size_t ws_chunk = workspace_for(dtype, rows_per_chunk, m);
+  // 256-byte aligned per-stream slices (the kernels use 16-byte vector accesses).
+  const size_t ws_chunk = (workspace_for(dtype, rows_per_chunk, m) + 255) & ~size_t(255);
   std::vector<void*> wss(2, nullptr);
   void* ws_all = nullptr;
   if (ws_chunk > 0) {

@@ -186,74 +186,135 @@ struct IoTraits<__nv_bfloat16> {
   static constexpr int VMAX = 3;
 };
 
+// Cache operators for global traffic: kNC = read-only path (ld.global.nc),
+// kStream = evict-first streaming (ld/st.global.cs: data touched once),
+// kL2 = cache in L2 only (ld/st.global.cg: the fused kernels' L2-resident
+// intermediate, never served from a possibly stale L1).
+enum class Cache : int { kNC = 0, kStream = 1, kL2 = 2, kL2Last = 3 };
+
+// kL2Last: L1-bypassing access with an L2 evict_last policy (createpolicy), for
+// intermediates that must survive in L2 while streaming traffic passes by.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float ld_l2last(const float* ptr) {
+  float v;
+  asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;"
+               : "=f"(v)
+               : "l"(ptr), "l"(l2_evict_last_policy()));
+  return v;
+}
+__device__ __forceinline__ float4 ld_l2last(const float4* ptr) {
+  float4 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(ptr), "l"(l2_evict_last_policy()));
+  return v;
+}
+__device__ __forceinline__ void st_l2last(float* ptr, float v) {
+  asm volatile("st.global.cg.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr), "f"(v),
+               "l"(l2_evict_last_policy())
+               : "memory");
+}
+__device__ __forceinline__ void st_l2last(float4* ptr, float4 v) {
+  asm volatile("st.global.cg.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(l2_evict_last_policy())
+               : "memory");
+}
+
+template <Cache CO, class V>
+__device__ __forceinline__ V gload(const V* p) {
+  if constexpr (CO == Cache::kNC)
+    return __ldg(p);
+  else if constexpr (CO == Cache::kStream)
+    return __ldcs(p);
+  else if constexpr (CO == Cache::kL2Last)
+    return ld_l2last(p);
+  else
+    return __ldcg(p);
+}
+template <Cache CO, class V>
+__device__ __forceinline__ void gstore(V* p, V v) {
+  if constexpr (CO == Cache::kStream)
+    __stcs(p, v);
+  else if constexpr (CO == Cache::kL2)
+    __stcg(p, v);
+  else if constexpr (CO == Cache::kL2Last)
+    st_l2last(p, v);
+  else
+    *p = v;
+}
+
 // Vector load of 2^VB consecutive T converted to C.
-template <class T, int VB>
+template <class T, int VB, Cache CO = Cache::kNC>
 struct VecIO;
 
-template <>
-struct VecIO<double, 0> {
-  __device__ __forceinline__ static void ld(const double* p, double* o) { o[0] = __ldg(p); }
-  __device__ __forceinline__ static void st(double* p, const double* v) { *p = v[0]; }
+template <Cache CO>
+struct VecIO<double, 0, CO> {
+  __device__ __forceinline__ static void ld(const double* p, double* o) { o[0] = gload<CO>(p); }
+  __device__ __forceinline__ static void st(double* p, const double* v) { gstore<CO>(p, v[0]); }
 };
-template <>
-struct VecIO<double, 1> {
+template <Cache CO>
+struct VecIO<double, 1, CO> {
   __device__ __forceinline__ static void ld(const double* p, double* o) {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 v = gload<CO>(reinterpret_cast<const double2*>(p));
     o[0] = v.x;
     o[1] = v.y;
   }
   __device__ __forceinline__ static void st(double* p, const double* v) {
-    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    gstore<CO>(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
   }
 };
-template <>
-struct VecIO<float, 0> {
-  __device__ __forceinline__ static void ld(const float* p, float* o) { o[0] = __ldg(p); }
-  __device__ __forceinline__ static void st(float* p, const float* v) { *p = v[0]; }
+template <Cache CO>
+struct VecIO<float, 0, CO> {
+  __device__ __forceinline__ static void ld(const float* p, float* o) { o[0] = gload<CO>(p); }
+  __device__ __forceinline__ static void st(float* p, const float* v) { gstore<CO>(p, v[0]); }
 };
-template <>
-struct VecIO<float, 1> {
+template <Cache CO>
+struct VecIO<float, 1, CO> {
   __device__ __forceinline__ static void ld(const float* p, float* o) {
-    const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+    const float2 v = gload<CO>(reinterpret_cast<const float2*>(p));
     o[0] = v.x;
     o[1] = v.y;
   }
   __device__ __forceinline__ static void st(float* p, const float* v) {
-    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    gstore<CO>(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
   }
 };
-template <>
-struct VecIO<float, 2> {
+template <Cache CO>
+struct VecIO<float, 2, CO> {
   __device__ __forceinline__ static void ld(const float* p, float* o) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 v = gload<CO>(reinterpret_cast<const float4*>(p));
     o[0] = v.x;
     o[1] = v.y;
     o[2] = v.z;
     o[3] = v.w;
   }
   __device__ __forceinline__ static void st(float* p, const float* v) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    gstore<CO>(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
   }
 };
 // bf16: 2^VB elements packed; converted to/from fp32 registers.
-template <int VB>
-struct VecIO<__nv_bfloat16, VB> {
+template <int VB, Cache CO>
+struct VecIO<__nv_bfloat16, VB, CO> {
   static constexpr int N = 1 << VB;
   __device__ __forceinline__ static void ld(const __nv_bfloat16* p, float* o) {
     if constexpr (VB == 0) {
-      o[0] = __bfloat162float(p[0]);
+      o[0] = __uint_as_float(((uint32_t)gload<CO>(reinterpret_cast<const unsigned short*>(p))) << 16);
     } else if constexpr (VB == 1) {
-      const uint32_t w = __ldg(reinterpret_cast<const unsigned int*>(p));
+      const uint32_t w = gload<CO>(reinterpret_cast<const unsigned int*>(p));
       o[0] = __uint_as_float(w << 16);
       o[1] = __uint_as_float(w & 0xffff0000u);
     } else if constexpr (VB == 2) {
-      const uint2 w = __ldg(reinterpret_cast<const uint2*>(p));
+      const uint2 w = gload<CO>(reinterpret_cast<const uint2*>(p));
       o[0] = __uint_as_float(w.x << 16);
       o[1] = __uint_as_float(w.x & 0xffff0000u);
       o[2] = __uint_as_float(w.y << 16);
       o[3] = __uint_as_float(w.y & 0xffff0000u);
     } else {
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(p));
+      const uint4 w = gload<CO>(reinterpret_cast<const uint4*>(p));
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -268,14 +329,15 @@ struct VecIO<__nv_bfloat16, VB> {
   }
   __device__ __forceinline__ static void st(__nv_bfloat16* p, const float* v) {
     if constexpr (VB == 0) {
-      p[0] = __float2bfloat16_rn(v[0]);
+      const __nv_bfloat16 h = __float2bfloat16_rn(v[0]);
+      gstore<CO>(reinterpret_cast<unsigned short*>(p), *reinterpret_cast<const unsigned short*>(&h));
     } else if constexpr (VB == 1) {
-      *reinterpret_cast<uint32_t*>(p) = pack2(v[0], v[1]);
+      gstore<CO>(reinterpret_cast<unsigned int*>(p), (unsigned int)pack2(v[0], v[1]));
     } else if constexpr (VB == 2) {
-      *reinterpret_cast<uint2*>(p) = make_uint2(pack2(v[0], v[1]), pack2(v[2], v[3]));
+      gstore<CO>(reinterpret_cast<uint2*>(p), make_uint2(pack2(v[0], v[1]), pack2(v[2], v[3])));
     } else {
-      *reinterpret_cast<uint4*>(p) =
-          make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
+      gstore<CO>(reinterpret_cast<uint4*>(p),
+                 make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7])));
     }
   }
 };
@@ -286,15 +348,15 @@ struct IoTraits<long long> {
   using C = long long;
   static constexpr int VMAX = 1;
 };
-template <>
-struct VecIO<long long, 0> {
-  __device__ __forceinline__ static void ld(const long long* p, long long* o) { o[0] = __ldg(p); }
-  __device__ __forceinline__ static void st(long long* p, const long long* v) { *p = v[0]; }
+template <Cache CO>
+struct VecIO<long long, 0, CO> {
+  __device__ __forceinline__ static void ld(const long long* p, long long* o) { o[0] = gload<CO>(p); }
+  __device__ __forceinline__ static void st(long long* p, const long long* v) { gstore<CO>(p, v[0]); }
 };
-template <>
-struct VecIO<long long, 1> {
+template <Cache CO>
+struct VecIO<long long, 1, CO> {
   __device__ __forceinline__ static void ld(const long long* p, long long* o) {
-    const longlong2 v = __ldg(reinterpret_cast<const longlong2*>(p));
+    const longlong2 v = gload<CO>(reinterpret_cast<const longlong2*>(p));
     o[0] = v.x;
     o[1] = v.y;
   }
@@ -302,7 +364,7 @@ struct VecIO<long long, 1> {
     longlong2 x;
     x.x = v[0];
     x.y = v[1];
-    *reinterpret_cast<longlong2*>(p) = x;
+    gstore<CO>(reinterpret_cast<longlong2*>(p), x);
   }
 };
 // Shared-memory vector access of 2^VB compute-type words.
@@ -443,7 +505,7 @@ __device__ __forceinline__ void shfl_butterfly(C (&v)[L::E], uint32_t tid) {
 // ---------------------------------------------------------------------------
 // Load a tile from global memory in layout L; element offset of tile bit k is
 // Map::pos(k) within the tile (tile base pointer already applied).
-template <class L, class Map, class T, class C>
+template <class L, class Map, Cache CO = Cache::kNC, class T, class C>
 __device__ __forceinline__ void load_global(const T* __restrict__ base, C (&v)[L::E], uint32_t tid) {
   constexpr int VB = vec_bits<L, Map>(IoTraits<T>::VMAX);
   const uint32_t tb = thr_off<L, Map>(tid);
@@ -451,7 +513,7 @@ __device__ __forceinline__ void load_global(const T* __restrict__ base, C (&v)[L
   for (int r = 0; r < L::E; ++r) {
     if (!vec_head<L, Map>(r, VB)) continue;
     C tmp[1 << VB];
-    VecIO<T, VB>::ld(base + (tb + reg_off<L, Map>(r)), tmp);
+    VecIO<T, VB, CO>::ld(base + (tb + reg_off<L, Map>(r)), tmp);
 #pragma unroll
     for (int q = 0; q < (1 << VB); ++q) v[vec_elem<L, Map>(r, q, VB)] = tmp[q];
   }
@@ -480,7 +542,7 @@ __device__ __forceinline__ void load_global_pred(const T* __restrict__ base, C (
 }
 
 // Store a tile to global memory, multiplying by `scale` when SCALE.
-template <class L, class Map, bool SCALE, class T, class C>
+template <class L, class Map, bool SCALE, Cache CO = Cache::kNC, class T, class C>
 __device__ __forceinline__ void store_global(T* __restrict__ base, const C (&v)[L::E], uint32_t tid,
                                              C scale) {
   constexpr int VB = vec_bits<L, Map>(IoTraits<T>::VMAX);
@@ -494,7 +556,7 @@ __device__ __forceinline__ void store_global(T* __restrict__ base, const C (&v)[
       const C x = v[vec_elem<L, Map>(r, q, VB)];
       tmp[q] = SCALE ? x * scale : x;
     }
-    VecIO<T, VB>::st(base + (tb + reg_off<L, Map>(r)), tmp);
+    VecIO<T, VB, CO>::st(base + (tb + reg_off<L, Map>(r)), tmp);
   }
 }
 

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstdint>
 #include <string>
@@ -13,6 +14,8 @@
 
 #include "../../include/chw_b200.h"
 #include "chw_kernels.cuh"
+#include "fused.cuh"
+#include "pipelined.cuh"
 
 namespace chwb {
 
@@ -29,6 +32,15 @@ void count_launch();
     cudaError_t e_ = (call);                            \
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
+
+// A/B switch for the pipelined kernels (CHW_B200_PIPELINE=0 disables them).
+inline bool pipeline_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CHW_B200_PIPELINE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 inline chw_status check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -51,10 +63,35 @@ chw_status prep_kernel(int smem) {
   return CHW_OK;
 }
 
+template <class P, bool SCALE>
+chw_status launch_k1p(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
+  constexpr auto k = k1p_kernel<P, SCALE>;
+  if (chw_status s = prep_kernel<k>(P::SMEM_BYTES)) return s;
+  static int occ_cache[64] = {0};
+  static int sms_cache[64] = {0};
+  int dev = 0;
+  if (chw_status s = current_device(&dev)) return s;
+  if (occ_cache[dev] == 0) {
+    int occ = 0, sms = 0;
+    CHW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, P::NT, P::SMEM_BYTES));
+    CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    occ_cache[dev] = std::max(1, occ);
+    sms_cache[dev] = sms;
+  }
+  const uint64_t tiles = (uint64_t)batch;  // one row per tile
+  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)occ_cache[dev] * sms_cache[dev]);
+  k<<<grid, P::NT, P::SMEM_BYTES, st>>>(in, out, tiles, scale);
+  return check_launch("k1p_kernel");
+}
+
 // Output-order variants of a plan are produced by swapping the output map.
 template <class T, int M, Scaling SC>
 chw_status launch_k1(const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale,
                      cudaStream_t st) {
+  if constexpr (std::is_same<T, float>::value && M == 12) {
+    if (pipeline_enabled())
+      return launch_k1p<PipeF32M12, SC == Scaling::kDeferred>(in, out, batch, scale, st);
+  }
   using Plan = typename K1Select<T, M>::Plan;
   constexpr int TB = Plan::kTB;
   constexpr int ROWS_PER_TILE = 1 << (TB - M);
@@ -109,11 +146,98 @@ chw_status launch_k4_from(const T* in, T* out, void* ws, int64_t batch,
   return CHW_OK;
 }
 
+// ---------------------------------------------------------------------------
+// K5 fused two-phase launcher (fused.cuh).
+// ---------------------------------------------------------------------------
+template <class F>
+struct FusedPlanGeom {
+  static FusedGeom make(int64_t batch) {
+    FusedGeom g{};
+    g.chunk_rows = (uint32_t)std::min<int64_t>(F::CHUNK_ROWS, batch);
+    g.nchunks = (uint32_t)((batch + g.chunk_rows - 1) / g.chunk_rows);
+    g.rows_last = (uint32_t)(batch - (int64_t)(g.nchunks - 1) * g.chunk_rows);
+    g.nA = g.chunk_rows * F::A_TILES_PER_ROW;
+    g.nB = g.chunk_rows * F::B_TILES_PER_ROW;
+    g.nslots = std::min<uint32_t>(F::NSLOTS, g.nchunks);
+    g.lag = std::min<uint32_t>(F::LAG, g.nslots - 1);
+    return g;
+  }
+  static size_t slot_bytes(const FusedGeom& g) {
+    return (size_t)g.nslots * g.chunk_rows * ((size_t)1 << F::M) * sizeof(typename F::W);
+  }
+  static size_t workspace(int64_t batch) {
+    if (batch <= 0) return 0;
+    const FusedGeom g = make(batch);
+    return slot_bytes(g) + 256 + sizeof(uint32_t) * (1 + 2 * (size_t)g.nchunks);
+  }
+};
+
+template <class F, bool SCALE>
+chw_status launch_fused(const typename F::T* in, typename F::T* out, void* ws, int64_t batch,
+                        typename F::W scale, cudaStream_t st) {
+  using G = FusedPlanGeom<F>;
+  const FusedGeom g = G::make(batch);
+  if ((uint64_t)g.nchunks * (g.nA + g.nB) > 0xfffffff0ull)
+    return fail(CHW_ERR_UNSUPPORTED, "chw_forward: batch too large for the fused schedule");
+  auto* slots = static_cast<typename F::W*>(ws);
+  auto* ctr = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ((G::slot_bytes(g) + 255) & ~size_t(255)));
+  CHW_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * (1 + 2 * (size_t)g.nchunks), st));
+  constexpr auto k = fused_kernel<F, SCALE>;
+  if (chw_status s = prep_kernel<k>(F::SMEM_BYTES)) return s;
+  static int occ_cache[64] = {0};
+  static int sms_cache[64] = {0};
+  int dev = 0;
+  if (chw_status s = current_device(&dev)) return s;
+  if (occ_cache[dev] == 0) {
+    int occ = 0, sms = 0;
+    CHW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, F::NT, F::SMEM_BYTES));
+    CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    occ_cache[dev] = std::max(1, occ);
+    sms_cache[dev] = sms;
+  }
+  const uint64_t total = (uint64_t)g.nchunks * (g.nA + g.nB);
+  const unsigned grid = (unsigned)std::min<uint64_t>(total, (uint64_t)occ_cache[dev] * sms_cache[dev]);
+  k<<<grid, F::NT, F::SMEM_BYTES, st>>>(in, out, slots, ctr, g, scale);
+  return check_launch("fused_kernel");
+}
+
+// Fused spec per (T, M), void when none exists (the K4 multi-pass path is used).
+template <class T, int M>
+struct FusedSelect {
+  using F = void;
+};
+template <>
+struct FusedSelect<float, 16> {
+  using F = FusedF32M16;
+};
+template <>
+struct FusedSelect<float, 24> {
+  using F = FusedF32M24;
+};
+
+template <class T, int MLO = Regime<T>::K1MAX + 1>
+size_t k4_workspace_m(int m, int64_t batch, size_t inter) {
+  if constexpr (MLO > kMaxM) {
+    return 0;
+  } else {
+    if (m != MLO) return k4_workspace_m<T, MLO + 1>(m, batch, inter);
+    using F = typename FusedSelect<T, MLO>::F;
+    if constexpr (!std::is_void<F>::value) {
+      return FusedPlanGeom<F>::workspace(batch);
+    } else {
+      return (size_t)batch * ((size_t)1 << m) * inter;
+    }
+  }
+}
+
 template <class T, int M, Scaling SC>
 chw_status launch_m(const T* in, T* out, void* ws, int64_t batch, typename IoTraits<T>::C scale,
                     cudaStream_t st) {
   if constexpr (M <= Regime<T>::K1MAX) {
     return launch_k1<T, M, SC>(in, out, batch, scale, st);
+  } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {
+    return launch_fused<typename FusedSelect<T, M>::F, SC == Scaling::kDeferred>(in, out, ws, batch,
+                                                                                 scale, st);
   } else {
     return launch_k4_from<T, M, SC, 0>(in, out, ws, batch, scale, st);
   }
@@ -138,12 +262,15 @@ const char* plan_name_m(int m) {
     if (m != M) return plan_name_m<T, M + 1>(m);
     if constexpr (M <= Regime<T>::K1MAX) {
       return K1Select<T, M>::kTuned ? "k1-tuned" : "k1-generic";
+    } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {
+      return "k5-fused-2phase";
     } else {
       static const std::string s = "k4-multipass:" + std::to_string(K4Sched<T, M>::NPASS);
       return s.c_str();
     }
   }
 }
+
 
 
 // Entry points per dtype, instantiated in inst_<dtype>_<regime>.cu:
@@ -156,6 +283,8 @@ chw_status forward_k4(int m, bool scaled_mode, const T* in, T* out, void* ws, in
                       typename IoTraits<T>::C scale, cudaStream_t st);
 template <class T>
 const char* plan_name(int m);
+template <class T>
+size_t k4_workspace(int m, int64_t batch);
 
 // scaled_mode: Orthonormal.  f64 scales per butterfly (bit-exact with the
 // reference); f32/bf16 defer to one multiply; int64 is never scaled.
@@ -193,6 +322,10 @@ struct ModeScaling {
   template <>                                                                                   \
   const char* plan_name<T>(int m) {                                                             \
     return plan_name_m<T>(m);                                                                   \
+  }                                                                                             \
+  template <>                                                                                   \
+  size_t k4_workspace<T>(int m, int64_t batch) {                                                \
+    return k4_workspace_m<T>(m, batch, sizeof(typename IoTraits<T>::C));                        \
   }
 
 }  // namespace chwb

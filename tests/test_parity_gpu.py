@@ -289,3 +289,49 @@ def test_launches_counted(cuda):
     before = chw.launch_count()
     _run(np.zeros((4, 1 << 12), np.float32), O, cuda, torch.float32)
     assert chw.launch_count() > before
+
+
+# ---------------------------------------------------------------------------
+# K5 fused two-phase kernel (m = 16, 24): several row chunks, a ragged last
+# chunk, in place and out of place, exact order probe, host path.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m,rows", [(16, 1), (16, 33), (16, 70), (16, 97), (24, 1), (24, 3)])
+def test_fused_chunks(cuda, m, rows):
+    import torch
+
+    chw = _chw()
+    rng = np.random.default_rng(900 + m + rows)
+    x = rng.standard_normal(size=(rows, 1 << m)).astype(np.float32)
+    t = torch.from_numpy(x).to(cuda)
+    out = torch.empty_like(t)
+    chw.chw_forward_batched_(t, chw.ScalingMode.Orthonormal, out=out)
+    inplace = t.clone()
+    chw.chw_forward_batched_(inplace, chw.ScalingMode.Orthonormal)
+    torch.cuda.synchronize()
+    assert torch.equal(out, inplace)
+    y = out.cpu().numpy()
+    ref = oracle.chw_batch(x.astype(np.float64), O)
+    for r in range(rows):
+        assert _rel_l2(y[r], ref[r]) <= F32_TOL
+    host = x.copy()
+    chw.chw_forward_host_(host, chw.ScalingMode.Orthonormal)
+    assert np.array_equal(host, y)
+    # order probe on integers (exact)
+    bound = 1 << max(0, 24 - m - 1)
+    xi = rng.integers(-bound, bound + 1, size=(rows, 1 << m), dtype=np.int64)
+    ti = torch.from_numpy(xi.astype(np.float32)).to(cuda)
+    chw.chw_forward_batched_(ti, chw.ScalingMode.Unnormalized)
+    torch.cuda.synchronize()
+    assert np.array_equal(ti.cpu().numpy().astype(np.int64), oracle.chw_batch(xi, U))
+
+
+def test_user_workspace_too_small_is_rejected(cuda):
+    import torch
+
+    chw = _chw()
+    x = torch.zeros(4, 1 << 16, device=cuda)
+    need = chw.workspace_bytes(chw.DTYPE_F32, 4, 1 << 16)
+    assert need > 0
+    ws = torch.empty(need - 1, dtype=torch.uint8, device=cuda)
+    with pytest.raises(ValueError, match="workspace"):
+        chw.chw_forward_batched_(x, chw.ScalingMode.Orthonormal, workspace=ws)
