@@ -147,6 +147,69 @@ struct FusedF32M16 {
 };
 
 // ---------------------------------------------------------------------------
+// m = 16, f32, 32 values per thread (128-thread tiles): twice the warps per SM
+// of FusedF32M16 for the latency-bound two-phase schedule.
+//   Pi: j2->0 j3->1 j0->2 j1->3 j5->4 j6->5 j7->6 j4->7, rest identity.
+// ---------------------------------------------------------------------------
+struct FusedF32M16b {
+  using T = float;
+  using W = float;
+  static constexpr int M = 16;
+  static constexpr int NT = 128;
+  static constexpr int MIN_BLOCKS = 4;
+  static constexpr int SMEM_BYTES = 4096 * 4;
+  static constexpr int A_TILES_PER_ROW = 16;
+  static constexpr int B_TILES_PER_ROW = 16;
+  static constexpr int CHUNK_ROWS = 32;
+  static constexpr int LAG = 4;     // > the per-CTA prefetch window, in chunk rounds
+  static constexpr int NSLOTS = 6;  // 6 x 8 MiB intermediate ring: L2-resident
+
+  struct A {
+    using L0 = Layout<BL<0, 1, 5, 6, 7>, BL<2, 3, 4, 8, 9, 10, 11>>;
+    using L1 = Layout<BL<2, 3, 4, 10, 11>, BL<0, 1, 5, 6, 7, 8, 9>>;
+    using S = Swz<5, 2, 6, 3, 7, 4>;
+    using MapOut = ListMap<2, 3, 0, 1, 7, 4, 5, 6, 8, 9, 10, 11>;
+    using B0 = BL<0, 1, 5, 6, 7>;
+    using B1 = BL<2, 3, 4>;
+  };
+  struct B {
+    using L0 = Layout<BL<0, 1, 9, 10, 11>, BL<2, 3, 4, 5, 6, 7, 8>>;
+    using L1 = Layout<BL<4, 5, 6, 7, 8>, BL<11, 10, 9, 0, 1, 2, 3>>;
+    using S = Swz<9, 2, 10, 3, 11, 4>;
+    using MapIn = ListMap<0, 1, 2, 3, 8, 9, 10, 11, 12, 13, 14, 15>;
+    using MapOut = ListMap<13, 12, 15, 14, 7, 6, 5, 4, 3, 2, 1, 0>;
+    using OuterAddr = BL<4, 5, 6, 7>;
+    using OuterOut = BL<10, 9, 8, 11>;
+    using B0 = BL<9, 10, 11>;
+    using B1 = BL<4, 5, 6, 7, 8>;
+  };
+
+  __device__ __forceinline__ static void a_offsets(uint32_t a, uint32_t& row, uint32_t& in_off,
+                                                   uint32_t& mid_off) {
+    row = a >> 4;
+    in_off = (a & 15u) << 12;
+    mid_off = in_off;
+  }
+  __device__ __forceinline__ static void b_offsets(uint32_t b, uint32_t& row, uint32_t& mid_off,
+                                                   uint32_t& out_off) {
+    row = b >> 4;
+    mid_off = deposit<typename B::OuterAddr>(b & 15u);
+    out_off = deposit<typename B::OuterOut>(b & 15u);
+  }
+  template <bool SCALE>
+  __device__ __forceinline__ static void run_a(const T* in, W* mid, W* sm, W scale) {
+    run_two_phase<typename A::L0, typename A::L1, typename A::S, typename A::B0, typename A::B1, -1, IdMap,
+                  typename A::MapOut, Cache::kStream, Cache::kL2, false>(in, mid, sm, scale);
+  }
+  template <bool SCALE>
+  __device__ __forceinline__ static void run_b(const W* mid, T* out, W* sm, W scale) {
+    run_two_phase<typename B::L0, typename B::L1, typename B::S, typename B::B0, typename B::B1, -1,
+                  typename B::MapIn, typename B::MapOut, Cache::kL2, Cache::kStream, SCALE>(mid, out, sm,
+                                                                                              scale);
+  }
+};
+
+// ---------------------------------------------------------------------------
 // m = 24, f32 (BASELINE cfg5): L = 2^13, H = 2^11.  256-thread CTAs, 64 KiB.
 //   A tile: 2 consecutive h-blocks of 8192 contiguous (k0..12 = j0..12, k13 = j13).
 //   B tile: 8 columns (intermediate address bits 0..2) x 2048 h.
@@ -217,38 +280,36 @@ struct FusedGeom {
   uint32_t rows_last;
 };
 
-// Work item w -> (is_a, chunk, tile).  Order: for t = 0.., A(t) then B(t - lag).
+// Work item w -> (is_a, chunk, tile).  Order: for rounds t = 0, 1, ...: the A
+// tiles of chunk t (if t < nchunks), then the B tiles of chunk t - lag (if
+// 0 <= t - lag < nchunks).  Rounds 0..lag-1 hold only A tiles, the last lag
+// rounds only B tiles.
 __device__ __forceinline__ bool decode_work(uint32_t w, const FusedGeom& g, bool& is_a, uint32_t& q,
                                             uint32_t& tile) {
   const uint32_t per = g.nA + g.nB;
-  if (g.lag == 0) {
-    q = w / per;
-    const uint32_t off = w - q * per;
-    if (q >= g.nchunks) return false;
-    is_a = off < g.nA;
-    tile = is_a ? off : off - g.nA;
-    return true;
-  }
-  // lag == 1: round 0 = A(0); rounds 1..nchunks-1 = A(t), B(t-1); last = B(nchunks-1)
-  if (w < g.nA) {
+  const uint32_t lag = g.lag < g.nchunks ? g.lag : g.nchunks;
+  const uint32_t head = lag * g.nA;  // rounds 0..lag-1
+  if (w < head) {
     is_a = true;
-    q = 0;
-    tile = w;
+    q = w / g.nA;
+    tile = w - q * g.nA;
     return true;
   }
-  const uint32_t w2 = w - g.nA;
-  const uint32_t t = 1 + w2 / per;
-  const uint32_t off = w2 - (t - 1) * per;
-  if (t < g.nchunks) {
+  const uint32_t w2 = w - head;
+  const uint32_t mid_rounds = g.nchunks - lag;  // rounds lag..nchunks-1: A(t), B(t-lag)
+  if (w2 < mid_rounds * per) {
+    const uint32_t r = w2 / per;
+    const uint32_t off = w2 - r * per;
     is_a = off < g.nA;
-    q = is_a ? t : t - 1;
+    q = is_a ? (lag + r) : r;
     tile = is_a ? off : off - g.nA;
     return true;
   }
-  if (t == g.nchunks && off < g.nB) {
+  const uint32_t w3 = w2 - mid_rounds * per;  // tail rounds: B of the last `lag` chunks
+  if (w3 < lag * g.nB) {
     is_a = false;
-    q = g.nchunks - 1;
-    tile = off;
+    q = mid_rounds + w3 / g.nB;
+    tile = w3 - (w3 / g.nB) * g.nB;
     return true;
   }
   return false;

@@ -16,6 +16,7 @@
 #include "chw_kernels.cuh"
 #include "fused.cuh"
 #include "pipelined.cuh"
+#include "warpspec.cuh"
 
 namespace chwb {
 
@@ -52,8 +53,10 @@ inline chw_status check_launch(const char* what) {
 template <auto Kern>
 chw_status prep_kernel(int smem) {
   // One-time (per kernel, per device) opt-in above 48 KiB of dynamic shared memory.
+  // (Static __shared__ counts against the 48 KiB default too, so opt in for
+  // anything near it.)
   static std::atomic<uint64_t> done_mask{0};
-  if (smem <= 48 * 1024) return CHW_OK;
+  if (smem <= 32 * 1024) return CHW_OK;
   int dev = 0;
   if (chw_status s = current_device(&dev)) return s;
   const uint64_t bit = 1ull << dev;
@@ -159,7 +162,7 @@ struct FusedPlanGeom {
     g.nA = g.chunk_rows * F::A_TILES_PER_ROW;
     g.nB = g.chunk_rows * F::B_TILES_PER_ROW;
     g.nslots = std::min<uint32_t>(F::NSLOTS, g.nchunks);
-    g.lag = std::min<uint32_t>(F::LAG, g.nslots - 1);
+    g.lag = std::min<uint32_t>(F::LAG, g.nslots - 1);  // slots must outnumber the lag
     return g;
   }
   static size_t slot_bytes(const FusedGeom& g) {
@@ -182,6 +185,47 @@ chw_status launch_fused(const typename F::T* in, typename F::T* out, void* ws, i
   auto* slots = static_cast<typename F::W*>(ws);
   auto* ctr = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ((G::slot_bytes(g) + 255) & ~size_t(255)));
   CHW_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * (1 + 2 * (size_t)g.nchunks), st));
+  if (const char* e = std::getenv("CHW_B200_FUSED"); !(e && e[0] == 'p')) {  // default: warp-specialized
+    constexpr auto kw = fused_ws_kernel<F, SCALE>;
+    constexpr int smem = FusedWS<F>::SMEM_BYTES;
+    if (chw_status s = prep_kernel<kw>(smem)) return s;
+    static int wocc[64] = {0};
+    static int wsms[64] = {0};
+    int wdev = 0;
+    if (chw_status s = current_device(&wdev)) return s;
+    if (wocc[wdev] == 0) {
+      int occ = 0, sms = 0;
+      CHW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw, F::NT + 32, smem));
+      CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wdev));
+      wocc[wdev] = std::max(1, occ);
+      wsms[wdev] = sms;
+    }
+    // All CTAs must be co-resident (items wait on items of other CTAs).
+    const uint64_t wtotal = (uint64_t)g.nchunks * (g.nA + g.nB);
+    const unsigned wgrid = (unsigned)std::min<uint64_t>(wtotal, (uint64_t)wocc[wdev] * wsms[wdev]);
+    kw<<<wgrid, F::NT + 32, smem, st>>>(in, out, slots, ctr, g, scale);
+    return check_launch("fused_ws_kernel");
+  }
+  if (pipeline_enabled()) {
+    constexpr auto kp = fused_p_kernel<F, SCALE>;
+    constexpr int smem = FusedPipe<F>::SMEM_BYTES;
+    if (chw_status s = prep_kernel<kp>(smem)) return s;
+    static int pocc[64] = {0};
+    static int psms[64] = {0};
+    int pdev = 0;
+    if (chw_status s = current_device(&pdev)) return s;
+    if (pocc[pdev] == 0) {
+      int occ = 0, sms = 0;
+      CHW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kp, F::NT, smem));
+      CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pdev));
+      pocc[pdev] = std::max(1, occ);
+      psms[pdev] = sms;
+    }
+    const uint64_t ptotal = (uint64_t)g.nchunks * (g.nA + g.nB);
+    const unsigned pgrid = (unsigned)std::min<uint64_t>(ptotal, (uint64_t)pocc[pdev] * psms[pdev]);
+    kp<<<pgrid, F::NT, smem, st>>>(in, out, slots, ctr, g, scale);
+    return check_launch("fused_p_kernel");
+  }
   constexpr auto k = fused_kernel<F, SCALE>;
   if (chw_status s = prep_kernel<k>(F::SMEM_BYTES)) return s;
   static int occ_cache[64] = {0};
@@ -208,7 +252,7 @@ struct FusedSelect {
 };
 template <>
 struct FusedSelect<float, 16> {
-  using F = FusedF32M16;
+  using F = FusedF32M16b;
 };
 template <>
 struct FusedSelect<float, 24> {
