@@ -17,6 +17,7 @@
 #include "fused.cuh"
 #include "pipelined.cuh"
 #include "warpspec.cuh"
+#include "cluster.cuh"
 
 namespace chwb {
 
@@ -245,6 +246,69 @@ chw_status launch_fused(const typename F::T* in, typename F::T* out, void* ws, i
   return check_launch("fused_kernel");
 }
 
+// K3 cluster launcher (cluster.cuh), f32 m = 16.
+template <bool SCALE, int XCH>
+chw_status launch_cluster_m16_x(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
+  using K = ClusterF32M16;
+  constexpr auto k = cluster_m16_kernel<SCALE, XCH>;
+  if (chw_status s = prep_kernel<k>(K::SMEM_BYTES)) return s;
+  static int ncl_cache[64] = {0};
+  int dev = 0;  // per-instantiation cache
+  if (chw_status s = current_device(&dev)) return s;
+  if (ncl_cache[dev] == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(K::CLUSTER * 1024, 1, 1);
+    cfg.blockDim = dim3(K::NT, 1, 1);
+    cfg.dynamicSmemBytes = K::SMEM_BYTES;
+    int ncl = 0;
+    CHW_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
+    ncl_cache[dev] = std::max(1, ncl);
+  }
+  const uint64_t clusters = std::min<uint64_t>((uint64_t)batch, (uint64_t)ncl_cache[dev]);
+  k<<<(unsigned)(clusters * K::CLUSTER), K::NT, K::SMEM_BYTES, st>>>(in, out, (uint64_t)batch, scale);
+  return check_launch("cluster_m16_kernel");
+}
+
+template <bool SCALE>
+chw_status launch_cluster_m16(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
+  static const int xch = [] {
+    const char* e = std::getenv("CHW_B200_XCH");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (xch == 3) {
+    using K = ClusterF32M16;
+    constexpr auto k = cluster_m16_pipe_kernel<SCALE>;
+    constexpr int smem = 2 * K::SMEM_BYTES;
+    if (chw_status s = prep_kernel<k>(smem)) return s;
+    static int ncl3[64] = {0};
+    int dev = 0;
+    if (chw_status s = current_device(&dev)) return s;
+    if (ncl3[dev] == 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(K::CLUSTER * 1024, 1, 1);
+      cfg.blockDim = dim3(K::NT, 1, 1);
+      cfg.dynamicSmemBytes = smem;
+      int ncl = 0;
+      CHW_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
+      ncl3[dev] = std::max(1, ncl);
+    }
+    const uint64_t clusters = std::min<uint64_t>((uint64_t)batch, (uint64_t)ncl3[dev]);
+    k<<<(unsigned)(clusters * K::CLUSTER), K::NT, smem, st>>>(in, out, (uint64_t)batch, scale);
+    return check_launch("cluster_m16_pipe_kernel");
+  }
+  if (xch == 0) return launch_cluster_m16_x<SCALE, 0>(in, out, batch, scale, st);
+  if (xch == 2) return launch_cluster_m16_x<SCALE, 2>(in, out, batch, scale, st);
+  return launch_cluster_m16_x<SCALE, 1>(in, out, batch, scale, st);
+}
+
+inline bool cluster_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CHW_B200_M16");
+    return !(e && e[0] == 'f');
+  }();
+  return on;
+}
+
 // Fused spec per (T, M), void when none exists (the K4 multi-pass path is used).
 template <class T, int M>
 struct FusedSelect {
@@ -280,6 +344,9 @@ chw_status launch_m(const T* in, T* out, void* ws, int64_t batch, typename IoTra
   if constexpr (M <= Regime<T>::K1MAX) {
     return launch_k1<T, M, SC>(in, out, batch, scale, st);
   } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {
+    if constexpr (std::is_same<T, float>::value && M == 16) {
+      if (cluster_enabled()) return launch_cluster_m16<SC == Scaling::kDeferred>(in, out, batch, scale, st);
+    }
     return launch_fused<typename FusedSelect<T, M>::F, SC == Scaling::kDeferred>(in, out, ws, batch,
                                                                                  scale, st);
   } else {
@@ -306,6 +373,8 @@ const char* plan_name_m(int m) {
     if (m != M) return plan_name_m<T, M + 1>(m);
     if constexpr (M <= Regime<T>::K1MAX) {
       return K1Select<T, M>::kTuned ? "k1-tuned" : "k1-generic";
+    } else if constexpr (std::is_same<T, float>::value && M == 16) {
+      return "k3-cluster-dsmem";
     } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {
       return "k5-fused-2phase";
     } else {
