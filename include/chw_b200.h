@@ -99,6 +99,19 @@ size_t chw_b200_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
 chw_status chw_b200_forward_host(const void* in_host, void* out_host, chw_dtype dtype,
                                  int64_t batch, uint64_t n, chw_mode mode);
 
+/* Batched Haar transform Psi_m <- chw::haar_forward_inplace
+ * (proj/include/chw/transforms.hpp:49-80): output row [s, d_coarsest, ...,
+ * d_finest], same operations and order as the reference (f64 bit-exact).
+ * dtype F64/F32/I64 (I64: Unnormalized only).  Device pointers, in == out
+ * allowed, asynchronous on `stream`.  Rows longer than 2^12 (f64) / 2^13
+ * (f32) use a workspace (NULL = library-managed). */
+chw_status chw_b200_haar_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                                 chw_mode mode, void* workspace, size_t workspace_bytes, void* stream);
+size_t chw_b200_haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
+/* Host-buffer Haar transform (synchronous). */
+chw_status chw_b200_haar_forward_host(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
+                                      uint64_t n, chw_mode mode);
+
 /* parallel_execute_inplace(x, workers, mode) on a DEVICE buffer of one signal.
  * Validation as parallel.cpp:84-91; the pool is replaced by the GPU. */
 chw_status chw_b200_parallel_execute(void* x, chw_dtype dtype, uint64_t n, int workers,

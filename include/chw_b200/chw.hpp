@@ -261,6 +261,36 @@ inline void normalize_inplace(std::span<double> x, int m, OpTally* tally = nullp
   if (tally) tally->multiplications += x.size();
 }
 
+// transforms.hpp:49-80 — the Haar transform Psi_m, on the GPU (bit-exact in f64).
+template <SampleValue T>
+void haar_forward_inplace(std::span<T> x, ScalingMode mode, OpTally* tally = nullptr, std::span<T> scratch = {}) {
+  (void)scratch;
+  detail::require_pow2(x.size(), "haar_forward");
+  detail::require_mode<T>(mode, "haar_forward");
+  if (x.size() > 1) {
+    if (chw_b200_is_device_pointer(x.data())) {
+      detail::raise(chw_b200_haar_forward(x.data(), x.data(), detail::dtype_of<T>(), 1, x.size(),
+                                          detail::mode_of(mode), nullptr, 0, nullptr));
+      detail::raise(chw_b200_stream_synchronize(nullptr));
+    } else {
+      detail::raise(chw_b200_haar_forward_host(x.data(), x.data(), detail::dtype_of<T>(), 1, x.size(),
+                                               detail::mode_of(mode)));
+    }
+  }
+  if (tally && x.size() > 1) {
+    std::uint64_t a = 0, m = 0;
+    detail::raise(chw_b200_op_tally(1, x.size(), detail::mode_of(mode), &a, &m));
+    tally->additions += a;
+    tally->multiplications += m;
+  }
+}
+
+template <SampleValue T>
+std::vector<T> haar_forward(std::vector<T> x, ScalingMode mode, OpTally* tally = nullptr) {
+  haar_forward_inplace(std::span<T>(x), mode, tally);
+  return x;
+}
+
 template <SampleValue T>
 std::vector<T> chw_forward(std::vector<T> x, ScalingMode mode, OpTally* tally = nullptr) {
   chw_forward_inplace(std::span<T>(x), mode, tally);

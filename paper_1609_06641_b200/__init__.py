@@ -60,6 +60,9 @@ EXPORTED_SYMBOLS = (
     "chw_b200_plan_name",
     "chw_b200_abi_version",
     "chw_b200_is_device_pointer",
+    "chw_b200_haar_forward",
+    "chw_b200_haar_workspace_bytes",
+    "chw_b200_haar_forward_host",
     "chw_b200_stream_synchronize",
 )
 
@@ -136,6 +139,13 @@ def _load() -> ctypes.CDLL:
     lib.chw_b200_plan_name.restype = c.c_char_p
     lib.chw_b200_abi_version.argtypes = []
     lib.chw_b200_abi_version.restype = c.c_int
+    lib.chw_b200_haar_forward.argtypes = [c.c_void_p, c.c_void_p, c.c_int, c.c_int64, c.c_uint64,
+                                          c.c_int, c.c_void_p, c.c_size_t, c.c_void_p]
+    lib.chw_b200_haar_forward.restype = c.c_int
+    lib.chw_b200_haar_workspace_bytes.argtypes = [c.c_int, c.c_int64, c.c_uint64]
+    lib.chw_b200_haar_workspace_bytes.restype = c.c_size_t
+    lib.chw_b200_haar_forward_host.argtypes = [c.c_void_p, c.c_void_p, c.c_int, c.c_int64, c.c_uint64, c.c_int]
+    lib.chw_b200_haar_forward_host.restype = c.c_int
     lib.chw_b200_is_device_pointer.argtypes = [c.c_void_p]
     lib.chw_b200_is_device_pointer.restype = c.c_int
     lib.chw_b200_stream_synchronize.argtypes = [c.c_void_p]
@@ -293,6 +303,53 @@ def chw_forward_host_(x, mode: ScalingMode = ScalingMode.Orthonormal, tally: Opt
     return x if out is None else out
 
 
+def haar_forward_batched_(x, mode: ScalingMode = ScalingMode.Unnormalized, tally: Optional[OpTally] = None,
+                          out=None, stream=None):
+    """Batched Haar transform Psi_m (transforms.hpp:49-80) over the last dim of
+    a contiguous CUDA tensor (float64, float32 or int64), in place or into `out`."""
+    torch = _torch()
+    if not x.is_cuda or not x.is_contiguous():
+        raise ValueError("haar_forward: expected a contiguous CUDA tensor")
+    n = int(x.shape[-1]) if x.dim() > 0 else 1
+    batch = x.numel() // n if n > 0 else 1
+    dst = x if out is None else out
+    with torch.cuda.device(x.device):
+        _check(lib.chw_b200_haar_forward(x.data_ptr(), dst.data_ptr(), dtype_code(x), batch, n, int(mode),
+                                         None, 0, _stream_ptr(stream)))
+    _tally_add(tally, 1, n, mode, batch)
+    return dst
+
+
+def haar_forward_inplace(x, mode: ScalingMode, tally: Optional[OpTally] = None, scratch=None):
+    """transforms.hpp:49-80 on a signal (1-D) or rows (last dim); CUDA tensors
+    in place on their device, host arrays staged through the device."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        haar_forward_batched_(x, mode, tally)
+        torch.cuda.current_stream().synchronize()
+        return x
+    import numpy as np
+
+    a = x.numpy() if isinstance(x, torch.Tensor) else x
+    if not isinstance(a, np.ndarray) or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("haar_forward: expected a contiguous array")
+    codes = {np.dtype(np.float64): DTYPE_F64, np.dtype(np.float32): DTYPE_F32, np.dtype(np.int64): DTYPE_I64}
+    if a.dtype not in codes:
+        raise ValueError(f"haar_forward: unsupported dtype {a.dtype}")
+    n = int(a.shape[-1]) if a.ndim else 1
+    batch = a.size // n if n else 1
+    _check(lib.chw_b200_haar_forward_host(a.ctypes.data, a.ctypes.data, codes[a.dtype], batch, n, int(mode)))
+    _tally_add(tally, 1, n, mode, batch)
+    return x
+
+
+def haar_forward(x, mode: ScalingMode, tally: Optional[OpTally] = None):
+    """transforms.hpp:214-218: by-value wrapper."""
+    torch = _torch()
+    y = x.clone() if isinstance(x, torch.Tensor) else __import__("numpy").array(x, copy=True)
+    return haar_forward_inplace(y, mode, tally)
+
+
 def parallel_execute_inplace(x, workers: int, mode: ScalingMode, tally: Optional[OpTally] = None):
     """parallel.hpp:16-17 / parallel.cpp:84-97: same validation and the same
     result as the serial transform; the thread pool is replaced by the GPU."""
@@ -389,6 +446,7 @@ def launch_count() -> int:
 __all__ = [
     "ScalingMode", "OpTally", "BlockSlice", "ResourceError", "ChwCudaError",
     "chw_forward", "chw_forward_inplace", "chw_forward_batched_", "chw_forward_host_",
+    "haar_forward", "haar_forward_inplace", "haar_forward_batched_",
     "parallel_execute", "parallel_execute_inplace", "normalize_inplace", "normalized",
     "stage_blocks", "bit_reverse", "natural_to_dyadic", "workspace_bytes", "plan_name",
     "launch_count", "lib", "LIB_PATH", "EXPORTED_SYMBOLS",

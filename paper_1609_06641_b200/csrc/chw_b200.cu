@@ -64,6 +64,12 @@ chw_status current_device(int* dev) {
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace chwb
 
+namespace chwb {
+size_t haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
+chw_status haar_forward_device(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                               chw_mode mode, void* ws, cudaStream_t st);
+}  // namespace chwb
+
 namespace {
 
 // Reference validation order and text: require_pow2 then require_mode
@@ -371,6 +377,59 @@ size_t chw_b200_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {
 chw_status chw_b200_forward_host(const void* in_host, void* out_host, chw_dtype dtype,
                                  int64_t batch, uint64_t n, chw_mode mode) {
   return host_impl(in_host, out_host, dtype, batch, n, mode);
+}
+
+size_t chw_b200_haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {
+  if (!is_pow2(n)) return 0;
+  return haar_workspace_bytes(dtype, batch, n);
+}
+
+chw_status chw_b200_haar_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                                 chw_mode mode, void* workspace, size_t workspace_bytes, void* stream) {
+  // transforms.hpp:51-52: require_pow2 then require_mode, "haar_forward" wording.
+  if (chw_status s = validate("haar_forward", dtype, n, mode)) return s;
+  if (dtype == CHW_BF16) return fail(CHW_ERR_UNSUPPORTED, "haar_forward: bf16 is not supported");
+  if (batch < 0) return fail(CHW_ERR_ARGUMENT, "haar_forward: negative batch");
+  if (batch == 0) return CHW_OK;
+  if (!in || !out) return fail(CHW_ERR_ARGUMENT, "haar_forward: null buffer");
+  const size_t need = haar_workspace_bytes(dtype, batch, n);
+  void* ws = workspace;
+  if (need > 0) {
+    if (ws == nullptr) {
+      int dev = 0;
+      if (chw_status s = current_device(&dev)) return s;
+      if (chw_status s = ensure_workspace(dev, need, &ws)) return s;
+    } else if (workspace_bytes < need) {
+      return fail(CHW_ERR_WORKSPACE, "haar_forward: workspace too small");
+    }
+  }
+  return haar_forward_device(in, out, dtype, batch, n, mode, ws, static_cast<cudaStream_t>(stream));
+}
+
+chw_status chw_b200_haar_forward_host(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
+                                      uint64_t n, chw_mode mode) {
+  if (chw_status s = validate("haar_forward", dtype, n, mode)) return s;
+  if (dtype == CHW_BF16) return fail(CHW_ERR_UNSUPPORTED, "haar_forward: bf16 is not supported");
+  if (batch < 0) return fail(CHW_ERR_ARGUMENT, "haar_forward: negative batch");
+  if (batch == 0) return CHW_OK;
+  if (!in_host || !out_host) return fail(CHW_ERR_ARGUMENT, "haar_forward: null buffer");
+  // Compatibility path (synchronous, unpipelined): one device copy of the batch.
+  const size_t bytes = (size_t)batch * (size_t)n * elem_size(dtype);
+  void* d = nullptr;
+  if (cudaMalloc(&d, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CHW_ERR_RESOURCE, "haar_forward: cannot allocate device buffer");
+  }
+  chw_status s = CHW_OK;
+  cudaError_t e = cudaMemcpy(d, in_host, bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpy");
+  if (s == CHW_OK) s = chw_b200_haar_forward(d, d, dtype, batch, n, mode, nullptr, 0, nullptr);
+  if (s == CHW_OK) {
+    e = cudaMemcpy(out_host, d, bytes, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpy");
+  }
+  cudaFree(d);
+  return s;
 }
 
 chw_status chw_b200_parallel_execute(void* x, chw_dtype dtype, uint64_t n, int workers,

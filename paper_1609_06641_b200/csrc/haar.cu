@@ -1,0 +1,190 @@
+// haar.cu — batched Haar wavelet transform Psi_m on the GPU.
+//
+// Replaces chw::haar_forward_inplace (proj/include/chw/transforms.hpp:49-80):
+// for len = n, n/2, ..., 2 the pairs (2i, 2i+1) of the current smooth prefix
+// give s = (a+b)k, d = (a-b)k (k = kInvSqrt2 in Orthonormal mode, 1 otherwise,
+// transforms.hpp:62-70); d goes to position len/2 + i, s to position i.  The
+// output row is [s, d_coarsest(1), ..., d_finest(n/2)].  Every operation is the
+// reference's, in the same order, so f64 results are bit-exact.
+//
+// Rows with n <= kSmemMax run all levels in one CTA per row out of shared
+// memory (one HBM read and write per element).  Longer rows first run global
+// "level" kernels (each halves the smooth prefix, ping-ponging it through the
+// workspace) until the prefix fits, then finish in shared memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <string>
+
+#include "launch.cuh"
+
+namespace chwb {
+namespace {
+
+template <class T>
+struct HaarOps;
+template <>
+struct HaarOps<double> {
+  __device__ static void bf(double a, double b, bool ortho, double& s, double& d) {
+    s = __dadd_rn(a, b);
+    d = __dsub_rn(a, b);
+    if (ortho) {
+      s = __dmul_rn(s, kInvSqrt2);
+      d = __dmul_rn(d, kInvSqrt2);
+    }
+  }
+};
+template <>
+struct HaarOps<float> {
+  __device__ static void bf(float a, float b, bool ortho, float& s, float& d) {
+    s = __fadd_rn(a, b);
+    d = __fsub_rn(a, b);
+    if (ortho) {
+      s = __fmul_rn(s, (float)kInvSqrt2);
+      d = __fmul_rn(d, (float)kInvSqrt2);
+    }
+  }
+};
+template <>
+struct HaarOps<long long> {
+  __device__ static void bf(long long a, long long b, bool, long long& s, long long& d) {
+    s = a + b;
+    d = a - b;
+  }
+};
+
+constexpr int kSmemMaxBytes = 64 * 1024;  // smooth prefix handled in shared memory
+
+// One CTA per row: levels len = n0 .. 2 on a prefix of length n0 held in smem.
+// `src` holds the prefix (row stride src_stride), results go to `dst` rows
+// (row stride dst_stride; d at [len/2, len), final s at [0]).
+template <class T>
+__global__ void haar_smem_kernel(const T* __restrict__ src, int64_t src_stride, T* __restrict__ dst,
+                                 int64_t dst_stride, uint32_t n0, bool ortho) {
+  extern __shared__ __align__(16) unsigned char hsm[];
+  T* a = reinterpret_cast<T*>(hsm);
+  T* b = a + n0;
+  const uint64_t row = blockIdx.x;
+  const T* s_in = src + row * src_stride;
+  T* out = dst + row * dst_stride;
+  for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) a[i] = s_in[i];
+  __syncthreads();
+  T* cur = a;
+  T* nxt = b;
+  for (uint32_t len = n0; len >= 2; len >>= 1) {
+    const uint32_t half = len >> 1;
+    for (uint32_t i = threadIdx.x; i < half; i += blockDim.x) {
+      T s, d;
+      HaarOps<T>::bf(cur[2 * i], cur[2 * i + 1], ortho, s, d);
+      nxt[i] = s;
+      out[half + i] = d;
+    }
+    __syncthreads();
+    T* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  if (threadIdx.x == 0) out[0] = cur[0];
+}
+
+// One level over all rows: pairs of the smooth prefix `src` (length len) ->
+// smooth `s_out` (len/2) and details at dst[row][len/2 + i].
+template <class T>
+__global__ void haar_level_kernel(const T* __restrict__ src, int64_t src_stride, T* __restrict__ s_out,
+                                  int64_t s_stride, T* __restrict__ dst, int64_t dst_stride, uint32_t len,
+                                  uint64_t rows, bool ortho) {
+  const uint32_t half = len >> 1;
+  const uint64_t total = rows * half;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t row = t / half;
+    const uint32_t i = (uint32_t)(t - row * half);
+    T s, d;
+    HaarOps<T>::bf(src[row * src_stride + 2 * i], src[row * src_stride + 2 * i + 1], ortho, s, d);
+    s_out[row * s_stride + i] = s;
+    dst[row * dst_stride + half + i] = d;
+  }
+}
+
+template <class T>
+chw_status haar_impl(const T* in, T* out, int64_t batch, uint64_t n, bool ortho, void* ws, cudaStream_t st) {
+  if (n == 1) {
+    if (in != out) CHW_CUDA(cudaMemcpyAsync(out, in, (size_t)batch * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    return CHW_OK;
+  }
+  const uint64_t smem_max = kSmemMaxBytes / (2 * sizeof(T));  // prefix + ping-pong half
+  const T* src = in;
+  int64_t src_stride = (int64_t)n;
+  uint64_t len = n;
+  T* bufs[2] = {static_cast<T*>(ws), static_cast<T*>(ws) + (size_t)batch * (n / 2)};
+  int which = 0;
+  if (len > smem_max && in == out) {
+    // In place: the first level may not overwrite unread input, so it writes
+    // its details to the workspace and they are copied into place after.
+    const uint64_t half = len / 2;
+    const uint64_t total = (uint64_t)batch * half;
+    const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+    haar_level_kernel<T><<<grid, 256, 0, st>>>(src, src_stride, bufs[0], (int64_t)half, bufs[1] - half,
+                                                (int64_t)half, (uint32_t)len, (uint64_t)batch, ortho);
+    if (chw_status s = check_launch("haar_level_kernel")) return s;
+    CHW_CUDA(cudaMemcpy2DAsync(out + half, n * sizeof(T), bufs[1], half * sizeof(T), half * sizeof(T),
+                               (size_t)batch, cudaMemcpyDeviceToDevice, st));
+    src = bufs[0];
+    src_stride = (int64_t)half;
+    len = half;
+    which = 1;
+  }
+  while (len > smem_max) {
+    T* s_out = bufs[which];
+    const uint64_t total = (uint64_t)batch * (len / 2);
+    const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+    haar_level_kernel<T><<<grid, 256, 0, st>>>(src, src_stride, s_out, (int64_t)(len / 2), out, (int64_t)n,
+                                                (uint32_t)len, (uint64_t)batch, ortho);
+    if (chw_status s = check_launch("haar_level_kernel")) return s;
+    src = s_out;
+    src_stride = (int64_t)(len / 2);
+    len >>= 1;
+    which ^= 1;
+  }
+  const int smem = (int)(len * sizeof(T) + (len / 2) * sizeof(T));
+  if (smem > 48 * 1024) {
+    CHW_CUDA(cudaFuncSetAttribute(haar_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  }
+  const int threads = (int)std::min<uint64_t>(256, std::max<uint64_t>(32, len / 2));
+  for (int64_t r0 = 0; r0 < batch; r0 += 0x7fffffff) {
+    const unsigned g = (unsigned)std::min<int64_t>(batch - r0, 0x7fffffff);
+    haar_smem_kernel<T><<<g, threads, smem, st>>>(src + r0 * src_stride, src_stride, out + r0 * (int64_t)n,
+                                                   (int64_t)n, (uint32_t)len, ortho);
+    if (chw_status s = check_launch("haar_smem_kernel")) return s;
+  }
+  return CHW_OK;
+}
+
+}  // namespace
+
+size_t haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {
+  const size_t es = (dtype == CHW_F32) ? 4 : 8;
+  const uint64_t smem_max = kSmemMaxBytes / (2 * es);
+  if (n <= smem_max || batch <= 0) return 0;
+  return 2 * (size_t)batch * (n / 2) * es;
+}
+
+chw_status haar_forward_device(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                               chw_mode mode, void* ws, cudaStream_t st) {
+  const bool ortho = (mode == CHW_ORTHONORMAL);
+  switch (dtype) {
+    case CHW_F64:
+      return haar_impl<double>(static_cast<const double*>(in), static_cast<double*>(out), batch, n, ortho, ws,
+                               st);
+    case CHW_F32:
+      return haar_impl<float>(static_cast<const float*>(in), static_cast<float*>(out), batch, n, ortho, ws, st);
+    case CHW_I64:
+      return haar_impl<long long>(static_cast<const long long*>(in), static_cast<long long*>(out), batch, n,
+                                  false, ws, st);
+    default:
+      return fail(CHW_ERR_UNSUPPORTED, "haar_forward: dtype not supported (f64, f32, int64)");
+  }
+}
+
+}  // namespace chwb

@@ -52,6 +52,10 @@ static void cpu_checks() {
   std::vector<I> two{1, 2};
   CHECK(throws_as<std::invalid_argument>([&] { chw_forward_inplace(std::span<I>(two), kO); },
                                          "orthonormal mode requires a floating-point signal"));
+  CHECK(throws_as<std::invalid_argument>([&] { haar_forward_inplace(std::span<I>(bad), kU); },
+                                         "haar_forward: length 3 is not a power of two"));
+  CHECK(throws_as<std::invalid_argument>([&] { haar_forward_inplace(std::span<I>(empty), kU); }));
+  CHECK(throws_as<std::invalid_argument>([&] { haar_forward_inplace(std::span<I>(two), kO); }));
   // transforms_test.cpp:88-110 — stage slices
   CHECK((stage_blocks(2, 1) == std::vector<BlockSlice>{{2, 2}}));
   CHECK((stage_blocks(4, 2) == std::vector<BlockSlice>{{4, 4}, {12, 4}}));
@@ -136,6 +140,24 @@ static void gpu_checks() {
     const auto y = chw_forward(x, kU, &tt);
     normalized(y, 4, &tt);
     CHECK(tt.additions == 64 && tt.multiplications == 16);
+  }
+  // transforms_test.cpp:27-45 — Haar KATs and counts on the GPU
+  {
+    OpTally th;
+    CHECK((haar_forward<I>({1, 0, 0, 0}, kU, &th) == std::vector<I>{1, 1, 1, 0}));
+    CHECK(th.additions == 6);
+    for (int m = 0; m <= 12; ++m) {
+      std::vector<I> x(std::size_t{1} << m);
+      for (auto& v : x) v = d(rng);
+      OpTally t2;
+      haar_forward_inplace(std::span<I>(x), kU, &t2);
+      CHECK(t2.additions == 2 * ((std::uint64_t{1} << m) - 1));
+    }
+    std::vector<double> x(16);
+    for (auto& v : x) v = u(rng);
+    OpTally t3;
+    haar_forward_inplace(std::span<double>(x), kO, &t3);
+    CHECK(t3.additions == 30 && t3.multiplications == 30);
   }
   // parallel_test.cpp:21-58 — equal to serial for every worker count, bitwise for doubles
   for (int m : {2, 5, 9, 13}) {

@@ -335,3 +335,62 @@ def test_user_workspace_too_small_is_rejected(cuda):
     ws = torch.empty(need - 1, dtype=torch.uint8, device=cuda)
     with pytest.raises(ValueError, match="workspace"):
         chw.chw_forward_batched_(x, chw.ScalingMode.Orthonormal, workspace=ws)
+
+
+# ---------------------------------------------------------------------------
+# a2: batched Haar transform Psi_m (transforms.hpp:49-80)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m", list(range(0, 19)))
+def test_haar_f64_bitexact(cuda, m):
+    import torch
+
+    chw = _chw()
+    rng = np.random.default_rng(1100 + m)
+    rows = max(1, min(9, (1 << 16) >> m))
+    x = rng.uniform(-1, 1, size=(rows, 1 << m))
+    for mode in (O, U):
+        t = torch.from_numpy(x).to(cuda)
+        out = torch.empty_like(t)
+        chw.haar_forward_batched_(t, chw.ScalingMode(mode), out=out)   # out of place
+        chw.haar_forward_batched_(t, chw.ScalingMode(mode))            # in place
+        torch.cuda.synchronize()
+        ref = np.stack([oracle.haar_forward(x[r], mode) for r in range(rows)])
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), ref.view(np.uint64))
+        assert np.array_equal(t.cpu().numpy().view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("m", [0, 1, 5, 12, 14, 17])
+def test_haar_i64_and_f32(cuda, m):
+    import torch
+
+    chw = _chw()
+    rng = np.random.default_rng(1200 + m)
+    xi = rng.integers(-1000, 1001, size=(3, 1 << m), dtype=np.int64)
+    ti = torch.from_numpy(xi).to(cuda)
+    chw.haar_forward_batched_(ti, chw.ScalingMode.Unnormalized)
+    torch.cuda.synchronize()
+    assert np.array_equal(ti.cpu().numpy(), np.stack([oracle.haar_forward(r, U) for r in xi]))
+    xf = rng.standard_normal(size=(3, 1 << m)).astype(np.float32)
+    tf = torch.from_numpy(xf).to(cuda)
+    chw.haar_forward_batched_(tf, chw.ScalingMode.Orthonormal)
+    torch.cuda.synchronize()
+    ref = np.stack([oracle.haar_forward(r.astype(np.float64), O) for r in xf])
+    for r in range(3):
+        assert _rel_l2(tf.cpu().numpy()[r], ref[r]) <= F32_TOL
+
+
+def test_haar_kats_and_validation(cuda):
+    # transforms_test.cpp:27-45, tally_test.cpp:30-36 and :70-77
+    chw = _chw()
+    t = chw.OpTally()
+    assert chw.haar_forward(np.array([7], np.int64), chw.ScalingMode.Unnormalized, t).tolist() == [7]
+    assert t.additions == 0
+    assert chw.haar_forward(np.array([1, 0, 0, 0], np.int64), chw.ScalingMode.Unnormalized, t).tolist() == [1, 1, 1, 0]
+    assert t.additions == 6
+    t = chw.OpTally()
+    chw.haar_forward(np.random.default_rng(4).uniform(-1, 1, 16), chw.ScalingMode.Orthonormal, t)
+    assert (t.additions, t.multiplications) == (30, 30)
+    with pytest.raises(ValueError, match="haar_forward: length 3 is not a power of two"):
+        chw.haar_forward(np.zeros(3, np.int64), chw.ScalingMode.Unnormalized)
+    with pytest.raises(ValueError, match="haar_forward: orthonormal mode requires a floating-point signal"):
+        chw.haar_forward(np.zeros(2, np.int64), chw.ScalingMode.Orthonormal)
