@@ -162,8 +162,11 @@ struct FusedPlanGeom {
     g.rows_last = (uint32_t)(batch - (int64_t)(g.nchunks - 1) * g.chunk_rows);
     g.nA = g.chunk_rows * F::A_TILES_PER_ROW;
     g.nB = g.chunk_rows * F::B_TILES_PER_ROW;
-    g.nslots = std::min<uint32_t>(F::NSLOTS, g.nchunks);
-    g.lag = std::min<uint32_t>(F::LAG, g.nslots - 1);  // slots must outnumber the lag
+    uint32_t nslots = F::NSLOTS, lag = F::LAG;
+    if (const char* e = std::getenv("CHW_B200_NSLOTS")) nslots = (uint32_t)std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("CHW_B200_LAG")) lag = (uint32_t)std::max(0, std::atoi(e));
+    g.nslots = std::min<uint32_t>(nslots, g.nchunks);
+    g.lag = std::min<uint32_t>(lag, g.nslots - 1);  // slots must outnumber the lag
     return g;
   }
   static size_t slot_bytes(const FusedGeom& g) {

@@ -97,8 +97,8 @@ struct TwoPhase {
 struct PipeF32M12 {
   static constexpr int M = 12;
   static constexpr int NT = 64;
-  static constexpr int STAGES = 2;
-  static constexpr int MIN_BLOCKS = 4;
+  static constexpr int STAGES = 4;      // measured sweep: 4 stages x 2 CTAs/SM best
+  static constexpr int MIN_BLOCKS = 2;
   using Item = TwoPhase<PlanF32M12::L0, PlanF32M12::L1, PlanF32M12::S, BL<0, 1, 8, 9, 10, 11>,
                         BL<2, 3, 4, 5, 6, 7>, -1, IdMap, RevMap<12>, Cache::kStream>;
   static constexpr int TILE = Item::TILE;
