@@ -88,8 +88,11 @@ chw_status chw_b200_forward_ordered(const void* in, void* out, chw_dtype dtype, 
                                     uint64_t n, chw_mode mode, chw_order order, void* workspace,
                                     size_t workspace_bytes, void* stream);
 
-/* Workspace the device call needs (0 for single-pass sizes). */
+/* Workspace the device call needs (0 for single-pass sizes), and for a call
+ * with an explicit order (NATURAL/SEQUENCY add one batch-sized buffer: the
+ * dyadic result is gathered into the requested order in one coalesced pass). */
 size_t chw_b200_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
+size_t chw_b200_workspace_bytes_ordered(chw_dtype dtype, int64_t batch, uint64_t n, chw_order order);
 
 /* Host-buffer call: copies `in_host` to the device, transforms, copies the
  * result to `out_host` (may equal in_host), and returns when done — the
@@ -111,6 +114,10 @@ size_t chw_b200_haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n)
 /* Host-buffer Haar transform (synchronous). */
 chw_status chw_b200_haar_forward_host(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
                                       uint64_t n, chw_mode mode);
+
+/* Host-buffer call with an explicit output order. */
+chw_status chw_b200_forward_host_ordered(const void* in_host, void* out_host, chw_dtype dtype,
+                                         int64_t batch, uint64_t n, chw_mode mode, chw_order order);
 
 /* parallel_execute_inplace(x, workers, mode) on a DEVICE buffer of one signal.
  * Validation as parallel.cpp:84-91; the pool is replaced by the GPU. */

@@ -21,7 +21,9 @@
 //   OpTally                          op_tally.hpp:12-22
 //   bit_reverse, natural_to_dyadic, dyadic_to_sequency, Permutation  orderings.hpp:16-90
 //   BlockSlice, stage_blocks         transforms.hpp:20-42
+//   haar_forward(_inplace)           transforms.hpp:49-80, 214-218
 //   chw_forward_inplace              transforms.hpp:126-143
+//   fwht_natural(_inplace), fwht_dyadic(_inplace)  transforms.hpp:147-185, 232-242
 //   normalize_inplace                transforms.hpp:202-210
 //   chw_forward                      transforms.hpp:226-230
 //   normalized                       transforms.hpp:250-260
@@ -152,15 +154,15 @@ inline void tally_chw(OpTally* tally, std::size_t n, ScalingMode mode, std::uint
 
 // rows x n contiguous values at `data` (host or device), in place, synchronous.
 template <class T>
-void run_rows(T* data, std::size_t rows, std::size_t n, ScalingMode mode) {
+void run_rows(T* data, std::size_t rows, std::size_t n, ScalingMode mode, chw_order order = CHW_ORDER_DYADIC) {
   if (rows == 0) return;
   if (chw_b200_is_device_pointer(data)) {
-    raise(chw_b200_forward(data, data, dtype_of<T>(), static_cast<std::int64_t>(rows), n,
-                           mode_of(mode), nullptr, 0, nullptr));
+    raise(chw_b200_forward_ordered(data, data, dtype_of<T>(), static_cast<std::int64_t>(rows), n,
+                                   mode_of(mode), order, nullptr, 0, nullptr));
     raise(chw_b200_stream_synchronize(nullptr));
   } else {
-    raise(chw_b200_forward_host(data, data, dtype_of<T>(), static_cast<std::int64_t>(rows), n,
-                                mode_of(mode)));
+    raise(chw_b200_forward_host_ordered(data, data, dtype_of<T>(), static_cast<std::int64_t>(rows), n,
+                                        mode_of(mode), order));
   }
 }
 
@@ -249,6 +251,37 @@ void chw_forward_batched_inplace(std::span<T> rows, std::size_t n, ScalingMode m
                                 " values is not a whole number of rows of " + std::to_string(n));
   if (n > 1) detail::run_rows(rows.data(), rows.size() / n, n, mode);
   detail::tally_chw(tally, n, mode, rows.size() / n);
+}
+
+// transforms.hpp:147-172 — natural (Sylvester) order WHT, on the GPU: the CHW
+// network without the final bit reversal; bitwise equal to the reference.
+template <SampleValue T>
+void fwht_natural_inplace(std::span<T> x, ScalingMode mode, OpTally* tally = nullptr) {
+  detail::require_pow2(x.size(), "fwht_natural");
+  detail::require_mode<T>(mode, "fwht_natural");
+  if (x.size() > 1) detail::run_rows(x.data(), 1, x.size(), mode, CHW_ORDER_NATURAL);
+  detail::tally_chw(tally, x.size(), mode, 1);
+}
+
+// transforms.hpp:177-185 — natural WHT + bit reversal: the dyadic transform.
+template <SampleValue T>
+void fwht_dyadic_inplace(std::span<T> x, ScalingMode mode, OpTally* tally = nullptr) {
+  detail::require_pow2(x.size(), "fwht_natural");
+  detail::require_mode<T>(mode, "fwht_natural");
+  if (x.size() > 1) detail::run_rows(x.data(), 1, x.size(), mode, CHW_ORDER_DYADIC);
+  detail::tally_chw(tally, x.size(), mode, 1);
+}
+
+template <SampleValue T>
+std::vector<T> fwht_natural(std::vector<T> x, ScalingMode mode, OpTally* tally = nullptr) {
+  fwht_natural_inplace(std::span<T>(x), mode, tally);
+  return x;
+}
+
+template <SampleValue T>
+std::vector<T> fwht_dyadic(std::vector<T> x, ScalingMode mode, OpTally* tally = nullptr) {
+  fwht_dyadic_inplace(std::span<T>(x), mode, tally);
+  return x;
 }
 
 inline void normalize_inplace(std::span<double> x, int m, OpTally* tally = nullptr) {

@@ -63,6 +63,8 @@ EXPORTED_SYMBOLS = (
     "chw_b200_haar_forward",
     "chw_b200_haar_workspace_bytes",
     "chw_b200_haar_forward_host",
+    "chw_b200_workspace_bytes_ordered",
+    "chw_b200_forward_host_ordered",
     "chw_b200_stream_synchronize",
 )
 
@@ -146,6 +148,11 @@ def _load() -> ctypes.CDLL:
     lib.chw_b200_haar_workspace_bytes.restype = c.c_size_t
     lib.chw_b200_haar_forward_host.argtypes = [c.c_void_p, c.c_void_p, c.c_int, c.c_int64, c.c_uint64, c.c_int]
     lib.chw_b200_haar_forward_host.restype = c.c_int
+    lib.chw_b200_workspace_bytes_ordered.argtypes = [c.c_int, c.c_int64, c.c_uint64, c.c_int]
+    lib.chw_b200_workspace_bytes_ordered.restype = c.c_size_t
+    lib.chw_b200_forward_host_ordered.argtypes = [c.c_void_p, c.c_void_p, c.c_int, c.c_int64, c.c_uint64,
+                                                  c.c_int, c.c_int]
+    lib.chw_b200_forward_host_ordered.restype = c.c_int
     lib.chw_b200_is_device_pointer.argtypes = [c.c_void_p]
     lib.chw_b200_is_device_pointer.restype = c.c_int
     lib.chw_b200_stream_synchronize.argtypes = [c.c_void_p]
@@ -250,6 +257,56 @@ def chw_forward_inplace(x, mode: ScalingMode = ScalingMode.Orthonormal, tally: O
         torch.cuda.current_stream().synchronize()  # reference calls are synchronous
         return x
     return chw_forward_host_(x, mode, tally)
+
+
+def _ordered_inplace(x, mode, tally, order):
+    torch = _torch()
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        chw_forward_batched_(x, mode, tally, order=order)
+        torch.cuda.current_stream().synchronize()
+        return x
+    t = torch.as_tensor(x)
+    d = t.cuda()
+    chw_forward_batched_(d, mode, tally, order=order)
+    res = d.cpu()
+    if isinstance(x, torch.Tensor):
+        x.copy_(res)
+    else:
+        import numpy as np
+
+        np.copyto(x, res.numpy())
+    return x
+
+
+def fwht_natural_inplace(x, mode: ScalingMode, tally: Optional[OpTally] = None):
+    """transforms.hpp:147-172: WHT in natural (Sylvester) order = the CHW
+    network without the final bit reversal (f2/f3)."""
+    return _ordered_inplace(x, mode, tally, ORDER_NATURAL)
+
+
+def fwht_natural(x, mode: ScalingMode, tally: Optional[OpTally] = None):
+    torch = _torch()
+    y = x.clone() if isinstance(x, torch.Tensor) else __import__("numpy").array(x, copy=True)
+    return fwht_natural_inplace(y, mode, tally)
+
+
+def fwht_dyadic_inplace(x, mode: ScalingMode, tally: Optional[OpTally] = None):
+    """transforms.hpp:177-185: natural WHT + bit reversal == chw_forward."""
+    return _ordered_inplace(x, mode, tally, ORDER_DYADIC)
+
+
+def fwht_dyadic(x, mode: ScalingMode, tally: Optional[OpTally] = None):
+    torch = _torch()
+    y = x.clone() if isinstance(x, torch.Tensor) else __import__("numpy").array(x, copy=True)
+    return fwht_dyadic_inplace(y, mode, tally)
+
+
+def chw_forward_sequency(x, mode: ScalingMode = ScalingMode.Orthonormal, tally: Optional[OpTally] = None):
+    """chw_forward followed by apply_permutation(dyadic_to_sequency(m), .)
+    (orderings.hpp:82-102, the CLI's --order sequency, chw_main.cpp:76-89)."""
+    torch = _torch()
+    y = x.clone() if isinstance(x, torch.Tensor) else __import__("numpy").array(x, copy=True)
+    return _ordered_inplace(y, mode, tally, ORDER_SEQUENCY)
 
 
 def chw_forward(x, mode: ScalingMode = ScalingMode.Orthonormal, tally: Optional[OpTally] = None):
@@ -447,6 +504,7 @@ __all__ = [
     "ScalingMode", "OpTally", "BlockSlice", "ResourceError", "ChwCudaError",
     "chw_forward", "chw_forward_inplace", "chw_forward_batched_", "chw_forward_host_",
     "haar_forward", "haar_forward_inplace", "haar_forward_batched_",
+    "fwht_natural", "fwht_natural_inplace", "fwht_dyadic", "fwht_dyadic_inplace", "chw_forward_sequency",
     "parallel_execute", "parallel_execute_inplace", "normalize_inplace", "normalized",
     "stage_blocks", "bit_reverse", "natural_to_dyadic", "workspace_bytes", "plan_name",
     "launch_count", "lib", "LIB_PATH", "EXPORTED_SYMBOLS",

@@ -65,6 +65,8 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace chwb
 
 namespace chwb {
+chw_status permute_order(const void* src, void* dst, size_t elem_bytes, chw_order order, int64_t batch, int m,
+                         cudaStream_t st);
 size_t haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
 chw_status haar_forward_device(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
                                chw_mode mode, void* ws, cudaStream_t st);
@@ -154,17 +156,28 @@ size_t workspace_for(chw_dtype dtype, int64_t batch, int m) {
   return 0;
 }
 
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t ordered_workspace(chw_dtype dtype, int64_t batch, int m, chw_order order) {
+  const size_t inner = workspace_for(dtype, batch, m);
+  if (order == CHW_ORDER_DYADIC || batch <= 0) return inner;
+  return align256(inner) + (size_t)batch * ((size_t)1 << m) * elem_size(dtype);
+}
+
+chw_status dyadic_impl(const void* in, void* out, chw_dtype dtype, int64_t batch, int m, chw_mode mode,
+                       void* ws, cudaStream_t st);
+
 chw_status forward_impl(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
                         chw_mode mode, chw_order order, void* workspace, size_t workspace_bytes,
                         cudaStream_t st) {
   if (chw_status s = validate("chw_forward", dtype, n, mode)) return s;
   if (batch < 0) return fail(CHW_ERR_ARGUMENT, "chw_forward: negative batch");
-  if (order != CHW_ORDER_DYADIC)
-    return fail(CHW_ERR_UNSUPPORTED, "chw_forward: only dyadic order is built in this version");
+  if (order != CHW_ORDER_DYADIC && order != CHW_ORDER_NATURAL && order != CHW_ORDER_SEQUENCY)
+    return fail(CHW_ERR_ARGUMENT, "chw_forward: unknown output order");
   if (batch == 0) return CHW_OK;
   if (!in || !out) return fail(CHW_ERR_ARGUMENT, "chw_forward: null buffer");
   const int m = level_of(n);
-  const size_t need = workspace_for(dtype, batch, m);
+  const size_t need = ordered_workspace(dtype, batch, m, order);
   void* ws = workspace;
   if (need > 0) {
     if (ws == nullptr) {
@@ -177,6 +190,15 @@ chw_status forward_impl(const void* in, void* out, chw_dtype dtype, int64_t batc
                                          " required");
     }
   }
+  if (order == CHW_ORDER_DYADIC) return dyadic_impl(in, out, dtype, batch, m, mode, ws, st);
+  // Other orders: dyadic result into the workspace, then one coalesced gather.
+  void* tmp = static_cast<char*>(ws) + align256(workspace_for(dtype, batch, m));
+  if (chw_status s = dyadic_impl(in, tmp, dtype, batch, m, mode, ws, st)) return s;
+  return permute_order(tmp, out, elem_size(dtype), order, batch, m, st);
+}
+
+chw_status dyadic_impl(const void* in, void* out, chw_dtype dtype, int64_t batch, int m, chw_mode mode,
+                       void* ws, cudaStream_t st) {
   const bool ortho = (mode == CHW_ORTHONORMAL);
   switch (dtype) {
     case CHW_F64: {
@@ -217,7 +239,7 @@ chw_status forward_impl(const void* in, void* out, chw_dtype dtype, int64_t batc
 // c-1 overlap (two copy engines + compute).
 // ---------------------------------------------------------------------------
 chw_status host_impl(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
-                     uint64_t n, chw_mode mode) {
+                     uint64_t n, chw_mode mode, chw_order order) {
   if (chw_status s = validate("chw_forward", dtype, n, mode)) return s;
   if (batch < 0) return fail(CHW_ERR_ARGUMENT, "chw_forward: negative batch");
   if (batch == 0) return CHW_OK;
@@ -256,7 +278,7 @@ chw_status host_impl(const void* in_host, void* out_host, chw_dtype dtype, int64
   }
   // Workspace for multi-pass sizes, one per stream.
   // 256-byte aligned per-stream slices (the kernels use 16-byte vector accesses).
-  const size_t ws_chunk = (workspace_for(dtype, rows_per_chunk, m) + 255) & ~size_t(255);
+  const size_t ws_chunk = (ordered_workspace(dtype, rows_per_chunk, m, order) + 255) & ~size_t(255);
   std::vector<void*> wss(2, nullptr);
   void* ws_all = nullptr;
   if (ws_chunk > 0) {
@@ -331,8 +353,7 @@ chw_status host_impl(const void* in_host, void* out_host, chw_dtype dtype, int64
       CHW_CUDA(cudaMemcpyAsync(d.dbuf[b], src + (size_t)r0 * row_bytes, bytes,
                                cudaMemcpyHostToDevice, st));
     }
-    if (chw_status s = forward_impl(d.dbuf[b], d.dbuf[b], dtype, rows, n, mode, CHW_ORDER_DYADIC,
-                                    wss[b], ws_chunk, st))
+    if (chw_status s = forward_impl(d.dbuf[b], d.dbuf[b], dtype, rows, n, mode, order, wss[b], ws_chunk, st))
       return s;
     void* h_out = (staged && !out_pinned) ? d.pinned[b] : dst + (size_t)r0 * row_bytes;
     CHW_CUDA(cudaMemcpyAsync(h_out, d.dbuf[b], bytes, cudaMemcpyDeviceToHost, st));
@@ -374,9 +395,19 @@ size_t chw_b200_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {
   return workspace_for(dtype, batch, level_of(n));
 }
 
+size_t chw_b200_workspace_bytes_ordered(chw_dtype dtype, int64_t batch, uint64_t n, chw_order order) {
+  if (!is_pow2(n)) return 0;
+  return ordered_workspace(dtype, batch, level_of(n), order);
+}
+
 chw_status chw_b200_forward_host(const void* in_host, void* out_host, chw_dtype dtype,
                                  int64_t batch, uint64_t n, chw_mode mode) {
-  return host_impl(in_host, out_host, dtype, batch, n, mode);
+  return host_impl(in_host, out_host, dtype, batch, n, mode, CHW_ORDER_DYADIC);
+}
+
+chw_status chw_b200_forward_host_ordered(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
+                                         uint64_t n, chw_mode mode, chw_order order) {
+  return host_impl(in_host, out_host, dtype, batch, n, mode, order);
 }
 
 size_t chw_b200_haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {

@@ -159,6 +159,20 @@ static void gpu_checks() {
     haar_forward_inplace(std::span<double>(x), kO, &t3);
     CHECK(t3.additions == 30 && t3.multiplications == 30);
   }
+  // transforms_test.cpp:145-170, orderings_test.cpp:79-84 — natural and dyadic FWHT
+  {
+    OpTally tf;
+    CHECK((fwht_natural<I>({1, 0}, kU, &tf) == std::vector<I>{1, 1}));
+    CHECK(tf.additions == 2);
+    const std::vector<I> x{0, 1, 0, 0};
+    const auto nat = fwht_natural(x, kU);
+    CHECK((std::vector<I>{nat[0], nat[2], nat[1], nat[3]} == chw_forward(x, kU)));
+    for (int m = 0; m <= 8; ++m) {
+      std::vector<I> y(std::size_t{1} << m);
+      for (auto& v : y) v = d(rng);
+      CHECK(fwht_dyadic(y, kU) == chw_forward(y, kU));
+    }
+  }
   // parallel_test.cpp:21-58 — equal to serial for every worker count, bitwise for doubles
   for (int m : {2, 5, 9, 13}) {
     std::vector<I> x(std::size_t{1} << m);

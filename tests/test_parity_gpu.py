@@ -394,3 +394,60 @@ def test_haar_kats_and_validation(cuda):
         chw.haar_forward(np.zeros(3, np.int64), chw.ScalingMode.Unnormalized)
     with pytest.raises(ValueError, match="haar_forward: orthonormal mode requires a floating-point signal"):
         chw.haar_forward(np.zeros(2, np.int64), chw.ScalingMode.Orthonormal)
+
+
+# ---------------------------------------------------------------------------
+# f2: natural and sequency orders (orderings_test.cpp:79-84, :35-65)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m", list(range(0, 21)))
+def test_orders_bitexact(cuda, m):
+    import torch
+
+    chw = _chw()
+    rng = np.random.default_rng(1300 + m)
+    rows = max(1, min(5, (1 << 15) >> m))
+    x = rng.uniform(-1, 1, size=(rows, 1 << m))
+    n = 1 << m
+    gray = np.array([i ^ (i >> 1) for i in range(n)])
+    for mode in (O, U):
+        nat = torch.from_numpy(x).to(cuda)
+        seq = nat.clone()
+        chw.chw_forward_batched_(nat, chw.ScalingMode(mode), order=chw.ORDER_NATURAL)
+        chw.chw_forward_batched_(seq, chw.ScalingMode(mode), order=chw.ORDER_SEQUENCY)
+        torch.cuda.synchronize()
+        ref_nat = np.stack([oracle.simple("fwht_natural", x[r], mode) for r in range(rows)])
+        ref_dy = oracle.chw_batch(x, mode)
+        assert np.array_equal(nat.cpu().numpy().view(np.uint64), ref_nat.view(np.uint64))
+        assert np.array_equal(seq.cpu().numpy().view(np.uint64), ref_dy[:, gray].view(np.uint64))
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16", "i64"])
+@pytest.mark.parametrize("m", [3, 10, 12, 16])
+def test_orders_other_dtypes(cuda, dt, m):
+    import torch
+
+    chw = _chw()
+    rng = np.random.default_rng(1400 + m)
+    xi = rng.integers(-1, 2, size=(4, 1 << m), dtype=np.int64)
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "i64": torch.int64}[dt]
+    if dt == "bf16" and m > 7:
+        pytest.skip("exact bf16 probe only for m <= 7")
+    dy = oracle.chw_batch(xi, U)
+    rev = np.array([oracle.bit_reverse(i, m) for i in range(1 << m)])
+    gray = np.array([i ^ (i >> 1) for i in range(1 << m)])
+    for order, ref in ((chw.ORDER_NATURAL, dy[:, rev]), (chw.ORDER_SEQUENCY, dy[:, gray])):
+        t = torch.from_numpy(xi).to(cuda).to(tdt)
+        chw.chw_forward_batched_(t, chw.ScalingMode.Unnormalized, order=order)
+        torch.cuda.synchronize()
+        assert np.array_equal(t.to(torch.float64).cpu().numpy().astype(np.int64), ref)
+
+
+def test_fwht_reference_api(cuda):
+    chw = _chw()
+    t = chw.OpTally()
+    assert chw.fwht_natural(np.array([1, 0], np.int64), chw.ScalingMode.Unnormalized, t).tolist() == [1, 1]
+    assert t.additions == 2
+    x = np.array([0, 1, 0, 0], np.int64)
+    assert chw.fwht_dyadic(x, chw.ScalingMode.Unnormalized).tolist() == [1, 1, -1, -1]
+    nat = chw.fwht_natural(x, chw.ScalingMode.Unnormalized)
+    assert nat[[0, 2, 1, 3]].tolist() == [1, 1, -1, -1]
