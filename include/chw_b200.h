@@ -56,7 +56,8 @@ typedef enum chw_status {
   CHW_ERR_WORKSPACE = 5,   /* caller workspace too small */
   CHW_ERR_CUDA = 6,        /* CUDA runtime error (text in last_error)  */
   CHW_ERR_NO_DEVICE = 7,   /* no CUDA device visible                   */
-  CHW_ERR_RESOURCE = 8     /* allocation failed                 -> chw::ResourceError */
+  CHW_ERR_RESOURCE = 8,    /* allocation failed                 -> chw::ResourceError */
+  CHW_ERR_STRUCTURE = 9    /* int64 haar_inverse of a non-forward output -> chw::StructureError */
 } chw_status;
 
 /* Order matches chw::ScalingMode (proj/include/chw/common.hpp:15). */
@@ -111,6 +112,20 @@ chw_status chw_b200_forward_host(const void* in_host, void* out_host, chw_dtype 
 chw_status chw_b200_haar_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
                                  chw_mode mode, void* workspace, size_t workspace_bytes, void* stream);
 size_t chw_b200_haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
+/* Batched inverse Haar transform <- chw::haar_inverse_inplace
+ * (proj/include/chw/transforms.hpp:85-120); same operations and order (f64
+ * bit-exact).  I64: an odd pair sum returns CHW_ERR_STRUCTURE (the reference's
+ * StructureError), so the I64 call synchronizes `stream` before returning. */
+chw_status chw_b200_haar_inverse(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                                 chw_mode mode, void* workspace, size_t workspace_bytes, void* stream);
+size_t chw_b200_haar_inverse_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
+
+/* Batched Haar-to-Walsh map <- chw::haar_walsh_forward_inplace
+ * (transforms.hpp:190-198): the dyadic WHT of each scale block
+ * [2^j, 2^(j+1)), j = 1..m-1, of every row.  Device buffers, in == out allowed. */
+chw_status chw_b200_haar_walsh_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                                       chw_mode mode, void* stream);
+
 /* Host-buffer Haar transform (synchronous). */
 chw_status chw_b200_haar_forward_host(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
                                       uint64_t n, chw_mode mode);

@@ -42,6 +42,7 @@ CHW_ERR_WORKSPACE = 5
 CHW_ERR_CUDA = 6
 CHW_ERR_NO_DEVICE = 7
 CHW_ERR_RESOURCE = 8
+CHW_ERR_STRUCTURE = 9
 
 DTYPE_F64, DTYPE_F32, DTYPE_BF16, DTYPE_I64 = 0, 1, 2, 3
 ORDER_DYADIC, ORDER_NATURAL, ORDER_SEQUENCY = 0, 1, 2
@@ -65,6 +66,9 @@ EXPORTED_SYMBOLS = (
     "chw_b200_haar_forward_host",
     "chw_b200_workspace_bytes_ordered",
     "chw_b200_forward_host_ordered",
+    "chw_b200_haar_inverse",
+    "chw_b200_haar_inverse_workspace_bytes",
+    "chw_b200_haar_walsh_forward",
     "chw_b200_stream_synchronize",
 )
 
@@ -78,6 +82,10 @@ class ScalingMode(enum.IntEnum):
 
 class ResourceError(RuntimeError):
     """chw::ResourceError (errors.hpp:32-36)."""
+
+
+class StructureError(RuntimeError):
+    """chw::StructureError (errors.hpp:15-19)."""
 
 
 class ChwCudaError(RuntimeError):
@@ -153,6 +161,14 @@ def _load() -> ctypes.CDLL:
     lib.chw_b200_forward_host_ordered.argtypes = [c.c_void_p, c.c_void_p, c.c_int, c.c_int64, c.c_uint64,
                                                   c.c_int, c.c_int]
     lib.chw_b200_forward_host_ordered.restype = c.c_int
+    lib.chw_b200_haar_inverse.argtypes = [c.c_void_p, c.c_void_p, c.c_int, c.c_int64, c.c_uint64,
+                                          c.c_int, c.c_void_p, c.c_size_t, c.c_void_p]
+    lib.chw_b200_haar_inverse.restype = c.c_int
+    lib.chw_b200_haar_inverse_workspace_bytes.argtypes = [c.c_int, c.c_int64, c.c_uint64]
+    lib.chw_b200_haar_inverse_workspace_bytes.restype = c.c_size_t
+    lib.chw_b200_haar_walsh_forward.argtypes = [c.c_void_p, c.c_void_p, c.c_int, c.c_int64, c.c_uint64,
+                                                c.c_int, c.c_void_p]
+    lib.chw_b200_haar_walsh_forward.restype = c.c_int
     lib.chw_b200_is_device_pointer.argtypes = [c.c_void_p]
     lib.chw_b200_is_device_pointer.restype = c.c_int
     lib.chw_b200_stream_synchronize.argtypes = [c.c_void_p]
@@ -171,6 +187,8 @@ def _check(status: int) -> None:
         raise ValueError(msg)
     if status == CHW_ERR_RESOURCE:
         raise ResourceError(msg)
+    if status == CHW_ERR_STRUCTURE:
+        raise StructureError(msg)
     if status == CHW_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
     raise ChwCudaError(f"{lib.chw_b200_status_string(status).decode()}: {msg}")
@@ -407,6 +425,71 @@ def haar_forward(x, mode: ScalingMode, tally: Optional[OpTally] = None):
     return haar_forward_inplace(y, mode, tally)
 
 
+def _device_rows(x):
+    """(tensor on device, writer-back) for CUDA tensors, numpy arrays or CPU tensors."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        return x, None
+    t = torch.as_tensor(x)
+    d = t.cuda()
+
+    def back():
+        res = d.cpu()
+        if isinstance(x, torch.Tensor):
+            x.copy_(res)
+        else:
+            import numpy as np
+
+            np.copyto(x, res.numpy())
+
+    return d, back
+
+
+def haar_inverse_inplace(x, mode: ScalingMode, scratch=None):
+    """transforms.hpp:85-120 (int64: StructureError on a non-forward output)."""
+    torch = _torch()
+    d, back = _device_rows(x)
+    n = int(d.shape[-1]) if d.dim() > 0 else 1
+    batch = d.numel() // n if n > 0 else 1
+    with torch.cuda.device(d.device):
+        _check(lib.chw_b200_haar_inverse(d.data_ptr(), d.data_ptr(), dtype_code(d), batch, n, int(mode),
+                                         None, 0, _stream_ptr(None)))
+    torch.cuda.current_stream().synchronize()
+    if back:
+        back()
+    return x
+
+
+def haar_inverse(y, mode: ScalingMode):
+    torch = _torch()
+    x = y.clone() if isinstance(y, torch.Tensor) else __import__("numpy").array(y, copy=True)
+    return haar_inverse_inplace(x, mode)
+
+
+def haar_walsh_forward_inplace(x, mode: ScalingMode, tally: Optional[OpTally] = None):
+    """transforms.hpp:190-198: dyadic WHT of each scale block [2^j, 2^(j+1))."""
+    torch = _torch()
+    d, back = _device_rows(x)
+    n = int(d.shape[-1]) if d.dim() > 0 else 1
+    batch = d.numel() // n if n > 0 else 1
+    with torch.cuda.device(d.device):
+        _check(lib.chw_b200_haar_walsh_forward(d.data_ptr(), d.data_ptr(), dtype_code(d), batch, n, int(mode),
+                                               _stream_ptr(None)))
+    torch.cuda.current_stream().synchronize()
+    if tally is not None and n > 2:
+        for j in range(1, level_of(n)):
+            _tally_add(tally, 0, 1 << j, mode, batch)
+    if back:
+        back()
+    return x
+
+
+def haar_walsh_forward(h, mode: ScalingMode, tally: Optional[OpTally] = None):
+    torch = _torch()
+    x = h.clone() if isinstance(h, torch.Tensor) else __import__("numpy").array(h, copy=True)
+    return haar_walsh_forward_inplace(x, mode, tally)
+
+
 def parallel_execute_inplace(x, workers: int, mode: ScalingMode, tally: Optional[OpTally] = None):
     """parallel.hpp:16-17 / parallel.cpp:84-97: same validation and the same
     result as the serial transform; the thread pool is replaced by the GPU."""
@@ -504,7 +587,8 @@ __all__ = [
     "ScalingMode", "OpTally", "BlockSlice", "ResourceError", "ChwCudaError",
     "chw_forward", "chw_forward_inplace", "chw_forward_batched_", "chw_forward_host_",
     "haar_forward", "haar_forward_inplace", "haar_forward_batched_",
-    "fwht_natural", "fwht_natural_inplace", "fwht_dyadic", "fwht_dyadic_inplace", "chw_forward_sequency",
+    "haar_inverse", "haar_inverse_inplace", "haar_walsh_forward", "haar_walsh_forward_inplace",
+    "StructureError", "fwht_natural", "fwht_natural_inplace", "fwht_dyadic", "fwht_dyadic_inplace", "chw_forward_sequency",
     "parallel_execute", "parallel_execute_inplace", "normalize_inplace", "normalized",
     "stage_blocks", "bit_reverse", "natural_to_dyadic", "workspace_bytes", "plan_name",
     "launch_count", "lib", "LIB_PATH", "EXPORTED_SYMBOLS",

@@ -68,6 +68,9 @@ namespace chwb {
 chw_status permute_order(const void* src, void* dst, size_t elem_bytes, chw_order order, int64_t batch, int m,
                          cudaStream_t st);
 size_t haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
+size_t haar_inverse_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
+chw_status haar_inverse_device(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                               chw_mode mode, void* ws, cudaStream_t st);
 chw_status haar_forward_device(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
                                chw_mode mode, void* ws, cudaStream_t st);
 }  // namespace chwb
@@ -463,6 +466,64 @@ chw_status chw_b200_haar_forward_host(const void* in_host, void* out_host, chw_d
   return s;
 }
 
+size_t chw_b200_haar_inverse_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {
+  if (!is_pow2(n)) return 0;
+  return haar_inverse_workspace_bytes(dtype, batch, n);
+}
+
+chw_status chw_b200_haar_inverse(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                                 chw_mode mode, void* workspace, size_t workspace_bytes, void* stream) {
+  // transforms.hpp:87-88: require_pow2 then require_mode, "haar_inverse" wording.
+  if (chw_status s = validate("haar_inverse", dtype, n, mode)) return s;
+  if (dtype == CHW_BF16) return fail(CHW_ERR_UNSUPPORTED, "haar_inverse: bf16 is not supported");
+  if (batch < 0) return fail(CHW_ERR_ARGUMENT, "haar_inverse: negative batch");
+  if (batch == 0) return CHW_OK;
+  if (!in || !out) return fail(CHW_ERR_ARGUMENT, "haar_inverse: null buffer");
+  const size_t need = haar_inverse_workspace_bytes(dtype, batch, n);
+  void* ws = workspace;
+  if (ws == nullptr) {
+    int dev = 0;
+    if (chw_status s = current_device(&dev)) return s;
+    if (chw_status s = ensure_workspace(dev, need, &ws)) return s;
+  } else if (workspace_bytes < need) {
+    return fail(CHW_ERR_WORKSPACE, "haar_inverse: workspace too small");
+  }
+  return haar_inverse_device(in, out, dtype, batch, n, mode, ws, static_cast<cudaStream_t>(stream));
+}
+
+chw_status chw_b200_haar_walsh_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                                       chw_mode mode, void* stream) {
+  // transforms.hpp:190-198: dyadic WHT of each scale block [2^j, 2^(j+1)), j = 1..m-1.
+  if (chw_status s = validate("haar_walsh_forward", dtype, n, mode)) return s;
+  if (batch < 0) return fail(CHW_ERR_ARGUMENT, "haar_walsh_forward: negative batch");
+  if (batch == 0) return CHW_OK;
+  if (!in || !out) return fail(CHW_ERR_ARGUMENT, "haar_walsh_forward: null buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t es = elem_size(dtype);
+  if (in != out) CHW_CUDA(cudaMemcpyAsync(out, in, (size_t)batch * n * es, cudaMemcpyDeviceToDevice, st));
+  const int m = level_of(n);
+  if (m < 2) return CHW_OK;
+  // Gather block j of every row into a contiguous [batch][2^j] buffer, run the
+  // batched dyadic kernel on it, scatter back.
+  const size_t tmp_bytes = (size_t)batch * (n / 2) * es;
+  int dev = 0;
+  if (chw_status s = current_device(&dev)) return s;
+  size_t inner = 0;
+  for (int j = 1; j <= m - 1; ++j) inner = std::max(inner, workspace_for(dtype, batch, j));
+  void* ws = nullptr;
+  if (chw_status s = ensure_workspace(dev, align256(tmp_bytes) + inner, &ws)) return s;
+  char* tmp = static_cast<char*>(ws);
+  void* inner_ws = tmp + align256(tmp_bytes);
+  char* o = static_cast<char*>(out);
+  for (int j = 1; j <= m - 1; ++j) {
+    const size_t blk = ((size_t)1 << j) * es;
+    CHW_CUDA(cudaMemcpy2DAsync(tmp, blk, o + blk, n * es, blk, (size_t)batch, cudaMemcpyDeviceToDevice, st));
+    if (chw_status s = dyadic_impl(tmp, tmp, dtype, batch, j, mode, inner_ws, st)) return s;
+    CHW_CUDA(cudaMemcpy2DAsync(o + blk, n * es, tmp, blk, blk, (size_t)batch, cudaMemcpyDeviceToDevice, st));
+  }
+  return CHW_OK;
+}
+
 chw_status chw_b200_parallel_execute(void* x, chw_dtype dtype, uint64_t n, int workers,
                                      chw_mode mode, void* stream) {
   // parallel.cpp:84-91: require_pow2, require_mode, then workers >= 1.
@@ -521,6 +582,8 @@ const char* chw_b200_status_string(chw_status s) {
       return "no CUDA device";
     case CHW_ERR_RESOURCE:
       return "resource allocation failed";
+    case CHW_ERR_STRUCTURE:
+      return "structural precondition failed";
   }
   return "unknown status";
 }

@@ -107,6 +107,159 @@ __global__ void haar_level_kernel(const T* __restrict__ src, int64_t src_stride,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Inverse (transforms.hpp:85-120): for len = 2..n, x[2i], x[2i+1] from the
+// smooth prefix s (length len/2) and the details d = x[len/2 + i]:
+//   float Orthonormal: (s+d)k, (s-d)k;  float Unnormalized: (s+d)/2, (s-d)/2;
+//   int64: sum = s+d must be even (else StructureError), sum/2, (s-d)/2.
+// ---------------------------------------------------------------------------
+template <class T>
+struct InvOps;
+template <>
+struct InvOps<double> {
+  __device__ static void op(double s, double d, bool ortho, double& a, double& b, int*) {
+    if (ortho) {
+      a = __dmul_rn(__dadd_rn(s, d), kInvSqrt2);
+      b = __dmul_rn(__dsub_rn(s, d), kInvSqrt2);
+    } else {
+      a = __ddiv_rn(__dadd_rn(s, d), 2.0);
+      b = __ddiv_rn(__dsub_rn(s, d), 2.0);
+    }
+  }
+};
+template <>
+struct InvOps<float> {
+  __device__ static void op(float s, float d, bool ortho, float& a, float& b, int*) {
+    if (ortho) {
+      a = __fmul_rn(__fadd_rn(s, d), (float)kInvSqrt2);
+      b = __fmul_rn(__fsub_rn(s, d), (float)kInvSqrt2);
+    } else {
+      a = __fdiv_rn(__fadd_rn(s, d), 2.0f);
+      b = __fdiv_rn(__fsub_rn(s, d), 2.0f);
+    }
+  }
+};
+template <>
+struct InvOps<long long> {
+  __device__ static void op(long long s, long long d, bool, long long& a, long long& b, int* err) {
+    const long long sum = s + d;
+    if (sum & 1) atomicExch(err, 1);
+    a = sum / 2;
+    b = (s - d) / 2;
+  }
+};
+
+// One CTA per row, levels len = 2..n0 on the prefix x[0..n0) held in smem.
+template <class T>
+__global__ void haar_inv_smem_kernel(const T* __restrict__ src, int64_t src_stride, T* __restrict__ dst,
+                                     int64_t dst_stride, uint32_t n0, bool ortho, int* err) {
+  extern __shared__ __align__(16) unsigned char hsm[];
+  T* x = reinterpret_cast<T*>(hsm);  // original prefix (s0 and the details)
+  T* p = x + n0;                     // smooth ping
+  T* q = p + n0;                     // smooth pong
+  const uint64_t row = blockIdx.x;
+  const T* in = src + row * src_stride;
+  T* out = dst + row * dst_stride;
+  for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) x[i] = in[i];
+  __syncthreads();
+  if (threadIdx.x == 0) p[0] = x[0];
+  __syncthreads();
+  T* cur = p;
+  T* nxt = q;
+  for (uint32_t len = 2; len <= n0; len <<= 1) {
+    const uint32_t half = len >> 1;
+    T* o = (len == n0) ? nullptr : nxt;
+    for (uint32_t i = threadIdx.x; i < half; i += blockDim.x) {
+      T a, b;
+      InvOps<T>::op(cur[i], x[half + i], ortho, a, b, err);
+      if (o) {
+        o[2 * i] = a;
+        o[2 * i + 1] = b;
+      } else {
+        out[2 * i] = a;
+        out[2 * i + 1] = b;
+      }
+    }
+    __syncthreads();
+    T* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+}
+
+// One level over all rows: smooth s (len/2) + details d_src[len/2 + i] -> dst (len).
+template <class T>
+__global__ void haar_inv_level_kernel(const T* __restrict__ s, int64_t s_stride, const T* __restrict__ d_src,
+                                      int64_t d_stride, int64_t d_off, T* __restrict__ dst, int64_t dst_stride,
+                                      uint32_t len, uint64_t rows, bool ortho, int* err) {
+  const uint32_t half = len >> 1;
+  const uint64_t total = rows * half;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t row = t / half;
+    const uint32_t i = (uint32_t)(t - row * half);
+    T a, b;
+    InvOps<T>::op(s[row * s_stride + i], d_src[row * d_stride + d_off + i], ortho, a, b, err);
+    dst[row * dst_stride + 2 * i] = a;
+    dst[row * dst_stride + 2 * i + 1] = b;
+  }
+}
+
+template <class T>
+chw_status haar_inv_impl(const T* in, T* out, int64_t batch, uint64_t n, bool ortho, void* ws, int* err,
+                         cudaStream_t st) {
+  if (n == 1) {
+    if (in != out) CHW_CUDA(cudaMemcpyAsync(out, in, (size_t)batch * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    return CHW_OK;
+  }
+  const uint64_t smem_max = kSmemMaxBytes / (3 * sizeof(T));
+  uint64_t n0 = 1;
+  while (n0 * 2 <= n && n0 * 2 <= smem_max) n0 *= 2;
+  const bool big = n0 < n;
+  T* bufs[2] = {static_cast<T*>(ws), static_cast<T*>(ws) + (size_t)batch * (n / 2)};
+  T* dcopy = static_cast<T*>(ws) + 2 * (size_t)batch * (n / 2);  // in-place: top-level details
+  const T* dsrc = in;
+  if (big && in == out) {
+    CHW_CUDA(cudaMemcpy2DAsync(dcopy, (n / 2) * sizeof(T), in + n / 2, n * sizeof(T), (n / 2) * sizeof(T),
+                               (size_t)batch, cudaMemcpyDeviceToDevice, st));
+  }
+  // Levels 2..n0 in shared memory.
+  T* first_dst = big ? bufs[0] : out;
+  const int64_t first_stride = big ? (int64_t)n0 : (int64_t)n;
+  const int smem = (int)(3 * n0 * sizeof(T));
+  if (smem > 48 * 1024)
+    CHW_CUDA(cudaFuncSetAttribute(haar_inv_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int threads = (int)std::min<uint64_t>(256, std::max<uint64_t>(32, n0 / 2));
+  for (int64_t r0 = 0; r0 < batch; r0 += 0x7fffffff) {
+    const unsigned g = (unsigned)std::min<int64_t>(batch - r0, 0x7fffffff);
+    haar_inv_smem_kernel<T><<<g, threads, smem, st>>>(in + r0 * (int64_t)n, (int64_t)n,
+                                                       first_dst + r0 * first_stride, first_stride, (uint32_t)n0,
+                                                       ortho, err);
+    if (chw_status s = check_launch("haar_inv_smem_kernel")) return s;
+  }
+  // Larger levels through global memory.
+  const T* s = bufs[0];
+  int64_t s_stride = (int64_t)n0;
+  int which = 1;
+  for (uint64_t len = 2 * n0; len <= n; len <<= 1) {
+    const bool last = (len == n);
+    T* dst = last ? out : bufs[which];
+    const int64_t dst_stride = last ? (int64_t)n : (int64_t)len;
+    const T* d = (last && in == out) ? dcopy : dsrc;
+    const int64_t d_stride = (last && in == out) ? (int64_t)(n / 2) : (int64_t)n;
+    const int64_t d_off = (last && in == out) ? 0 : (int64_t)(len / 2);
+    const uint64_t total = (uint64_t)batch * (len / 2);
+    const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+    haar_inv_level_kernel<T><<<grid, 256, 0, st>>>(s, s_stride, d, d_stride, d_off, dst, dst_stride,
+                                                    (uint32_t)len, (uint64_t)batch, ortho, err);
+    if (chw_status r = check_launch("haar_inv_level_kernel")) return r;
+    s = dst;
+    s_stride = dst_stride;
+    which ^= 1;
+  }
+  return CHW_OK;
+}
+
 template <class T>
 chw_status haar_impl(const T* in, T* out, int64_t batch, uint64_t n, bool ortho, void* ws, cudaStream_t st) {
   if (n == 1) {
@@ -162,6 +315,48 @@ chw_status haar_impl(const T* in, T* out, int64_t batch, uint64_t n, bool ortho,
 }
 
 }  // namespace
+
+size_t haar_inverse_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {
+  const size_t es = (dtype == CHW_F32) ? 4 : 8;
+  const uint64_t smem_max = kSmemMaxBytes / (3 * es);
+  if (n <= smem_max || batch <= 0) return 256;  // error flag
+  return 256 + 3 * (size_t)batch * (n / 2) * es;
+}
+
+chw_status haar_inverse_device(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
+                               chw_mode mode, void* ws, cudaStream_t st) {
+  // ws layout: [0, 256) error flag, then the level buffers.
+  int* err = static_cast<int*>(ws);
+  void* bufs = static_cast<char*>(ws) + 256;
+  CHW_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  const bool ortho = (mode == CHW_ORTHONORMAL);
+  chw_status s = CHW_OK;
+  switch (dtype) {
+    case CHW_F64:
+      s = haar_inv_impl<double>(static_cast<const double*>(in), static_cast<double*>(out), batch, n, ortho, bufs,
+                                err, st);
+      break;
+    case CHW_F32:
+      s = haar_inv_impl<float>(static_cast<const float*>(in), static_cast<float*>(out), batch, n, ortho, bufs,
+                               err, st);
+      break;
+    case CHW_I64:
+      s = haar_inv_impl<long long>(static_cast<const long long*>(in), static_cast<long long*>(out), batch, n,
+                                   false, bufs, err, st);
+      if (s == CHW_OK) {
+        // The reference throws StructureError on an odd pair sum
+        // (transforms.hpp:110-114): the integer inverse is synchronous.
+        int h = 0;
+        CHW_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CHW_CUDA(cudaStreamSynchronize(st));
+        if (h) s = fail(CHW_ERR_STRUCTURE, "haar_inverse: signal is not an integer forward-transform output");
+      }
+      break;
+    default:
+      s = fail(CHW_ERR_UNSUPPORTED, "haar_inverse: dtype not supported (f64, f32, int64)");
+  }
+  return s;
+}
 
 size_t haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {
   const size_t es = (dtype == CHW_F32) ? 4 : 8;

@@ -451,3 +451,55 @@ def test_fwht_reference_api(cuda):
     assert chw.fwht_dyadic(x, chw.ScalingMode.Unnormalized).tolist() == [1, 1, -1, -1]
     nat = chw.fwht_natural(x, chw.ScalingMode.Unnormalized)
     assert nat[[0, 2, 1, 3]].tolist() == [1, 1, -1, -1]
+
+
+# ---------------------------------------------------------------------------
+# f3: Haar inverse and Haar-Walsh (transforms_test.cpp:59-75, :172-192)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m", list(range(0, 18)))
+def test_haar_inverse_bitexact(cuda, m):
+    chw = _chw()
+    rng = np.random.default_rng(1500 + m)
+    rows = max(1, min(4, (1 << 15) >> m))
+    x = rng.uniform(-1, 1, size=(rows, 1 << m))
+    for mode in (O, U):
+        y = x.copy()
+        chw.haar_inverse_inplace(y, chw.ScalingMode(mode))
+        ref = np.stack([oracle.simple("haar_inverse", x[r], mode) for r in range(rows)])
+        assert np.array_equal(y.view(np.uint64), ref.view(np.uint64))
+    xi = rng.integers(-1000, 1001, size=(rows, 1 << m), dtype=np.int64)
+    h = np.stack([oracle.haar_forward(r, U) for r in xi])
+    back = chw.haar_inverse(h, chw.ScalingMode.Unnormalized)
+    assert np.array_equal(back, xi)  # integer round trip is exact
+
+
+def test_haar_inverse_structure_error(cuda):
+    chw = _chw()
+    assert chw.haar_inverse(np.array([5], np.int64), chw.ScalingMode.Unnormalized).tolist() == [5]
+    assert chw.haar_inverse(chw.haar_forward(np.array([1, 2, 3, 4], np.int64), chw.ScalingMode.Unnormalized),
+                            chw.ScalingMode.Unnormalized).tolist() == [1, 2, 3, 4]
+    with pytest.raises(chw.StructureError, match="not an integer forward-transform output"):
+        chw.haar_inverse(np.array([1, 0], np.int64), chw.ScalingMode.Unnormalized)
+    xf = np.random.default_rng(33).uniform(-1, 1, 64)
+    rt = chw.haar_inverse(chw.haar_forward(xf, chw.ScalingMode.Orthonormal), chw.ScalingMode.Orthonormal)
+    assert np.max(np.abs(rt - xf)) <= 1e-12
+
+
+@pytest.mark.parametrize("m", list(range(0, 17)))
+def test_haar_walsh(cuda, golden, m):
+    chw = _chw()
+    rng = np.random.default_rng(1600 + m)
+    x = rng.integers(-1000, 1001, size=(3, 1 << m), dtype=np.int64)
+    got = chw.haar_walsh_forward(x, chw.ScalingMode.Unnormalized)
+    ref = np.stack([oracle.simple("haar_walsh_forward", r, U) for r in x])
+    assert np.array_equal(got, ref)
+    # composition: haar_walsh(haar(x)) == chw(x) (transforms_test.cpp:181-184)
+    h = chw.haar_forward(x, chw.ScalingMode.Unnormalized)
+    assert np.array_equal(chw.haar_walsh_forward(h, chw.ScalingMode.Unnormalized), oracle.chw_batch(x, U))
+    if m == 7:
+        assert np.array_equal(chw.haar_walsh_forward(golden["haarwalsh_m7_in"], chw.ScalingMode.Unnormalized),
+                              golden["haarwalsh_m7_dense"])
+    xf = rng.uniform(-1, 1, size=(2, 1 << m))
+    gf = chw.haar_walsh_forward(xf, chw.ScalingMode.Orthonormal)
+    rf = np.stack([oracle.simple("haar_walsh_forward", r, O) for r in xf])
+    assert np.array_equal(gf.view(np.uint64), rf.view(np.uint64))
