@@ -126,6 +126,11 @@ size_t chw_b200_haar_inverse_workspace_bytes(chw_dtype dtype, int64_t batch, uin
 chw_status chw_b200_haar_walsh_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
                                        chw_mode mode, void* stream);
 
+/* Host-buffer variants (synchronous). */
+chw_status chw_b200_haar_inverse_host(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
+                                      uint64_t n, chw_mode mode);
+chw_status chw_b200_haar_walsh_forward_host(const void* in_host, void* out_host, chw_dtype dtype,
+                                            int64_t batch, uint64_t n, chw_mode mode);
 /* Host-buffer Haar transform (synchronous). */
 chw_status chw_b200_haar_forward_host(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
                                       uint64_t n, chw_mode mode);

@@ -22,6 +22,8 @@
 //   bit_reverse, natural_to_dyadic, dyadic_to_sequency, Permutation  orderings.hpp:16-90
 //   BlockSlice, stage_blocks         transforms.hpp:20-42
 //   haar_forward(_inplace)           transforms.hpp:49-80, 214-218
+//   haar_inverse(_inplace)           transforms.hpp:85-120, 220-224
+//   haar_walsh_forward(_inplace)     transforms.hpp:190-198, 244-248
 //   chw_forward_inplace              transforms.hpp:126-143
 //   fwht_natural(_inplace), fwht_dyadic(_inplace)  transforms.hpp:147-185, 232-242
 //   normalize_inplace                transforms.hpp:202-210
@@ -316,6 +318,56 @@ void haar_forward_inplace(std::span<T> x, ScalingMode mode, OpTally* tally = nul
     tally->additions += a;
     tally->multiplications += m;
   }
+}
+
+// transforms.hpp:85-120 — inverse Haar (int64: StructureError on a signal that
+// is not an integer forward-transform output).
+template <SampleValue T>
+void haar_inverse_inplace(std::span<T> x, ScalingMode mode, std::span<T> scratch = {}) {
+  (void)scratch;
+  detail::require_pow2(x.size(), "haar_inverse");
+  detail::require_mode<T>(mode, "haar_inverse");
+  if (x.size() < 2) return;
+  chw_status s;
+  if (chw_b200_is_device_pointer(x.data())) {
+    s = chw_b200_haar_inverse(x.data(), x.data(), detail::dtype_of<T>(), 1, x.size(), detail::mode_of(mode),
+                              nullptr, 0, nullptr);
+    if (s == CHW_OK) s = chw_b200_stream_synchronize(nullptr);
+  } else {
+    s = chw_b200_haar_inverse_host(x.data(), x.data(), detail::dtype_of<T>(), 1, x.size(), detail::mode_of(mode));
+  }
+  if (s == CHW_ERR_STRUCTURE) throw StructureError(chw_b200_last_error());
+  detail::raise(s);
+}
+
+template <SampleValue T>
+std::vector<T> haar_inverse(std::vector<T> y, ScalingMode mode) {
+  haar_inverse_inplace(std::span<T>(y), mode);
+  return y;
+}
+
+// transforms.hpp:190-198 — dyadic WHT of each scale block [2^j, 2^(j+1)).
+template <SampleValue T>
+void haar_walsh_forward_inplace(std::span<T> x, ScalingMode mode, OpTally* tally = nullptr) {
+  detail::require_pow2(x.size(), "haar_walsh_forward");
+  detail::require_mode<T>(mode, "haar_walsh_forward");
+  if (x.size() >= 4) {
+    if (chw_b200_is_device_pointer(x.data())) {
+      detail::raise(chw_b200_haar_walsh_forward(x.data(), x.data(), detail::dtype_of<T>(), 1, x.size(),
+                                                detail::mode_of(mode), nullptr));
+      detail::raise(chw_b200_stream_synchronize(nullptr));
+    } else {
+      detail::raise(chw_b200_haar_walsh_forward_host(x.data(), x.data(), detail::dtype_of<T>(), 1, x.size(),
+                                                     detail::mode_of(mode)));
+    }
+  }
+  for (int j = 1; j <= level_of(x.size()) - 1; ++j) detail::tally_chw(tally, std::size_t{1} << j, mode, 1);
+}
+
+template <SampleValue T>
+std::vector<T> haar_walsh_forward(std::vector<T> h, ScalingMode mode, OpTally* tally = nullptr) {
+  haar_walsh_forward_inplace(std::span<T>(h), mode, tally);
+  return h;
 }
 
 template <SampleValue T>

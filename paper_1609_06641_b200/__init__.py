@@ -69,6 +69,8 @@ EXPORTED_SYMBOLS = (
     "chw_b200_haar_inverse",
     "chw_b200_haar_inverse_workspace_bytes",
     "chw_b200_haar_walsh_forward",
+    "chw_b200_haar_inverse_host",
+    "chw_b200_haar_walsh_forward_host",
     "chw_b200_stream_synchronize",
 )
 
@@ -169,6 +171,9 @@ def _load() -> ctypes.CDLL:
     lib.chw_b200_haar_walsh_forward.argtypes = [c.c_void_p, c.c_void_p, c.c_int, c.c_int64, c.c_uint64,
                                                 c.c_int, c.c_void_p]
     lib.chw_b200_haar_walsh_forward.restype = c.c_int
+    for name in ("chw_b200_haar_inverse_host", "chw_b200_haar_walsh_forward_host"):
+        getattr(lib, name).argtypes = [c.c_void_p, c.c_void_p, c.c_int, c.c_int64, c.c_uint64, c.c_int]
+        getattr(lib, name).restype = c.c_int
     lib.chw_b200_is_device_pointer.argtypes = [c.c_void_p]
     lib.chw_b200_is_device_pointer.restype = c.c_int
     lib.chw_b200_stream_synchronize.argtypes = [c.c_void_p]

@@ -378,6 +378,36 @@ chw_status host_impl(const void* in_host, void* out_host, chw_dtype dtype, int64
 
 }  // namespace
 
+namespace {
+// Synchronous host-buffer wrapper for the secondary transforms (compatibility
+// path: one device copy of the batch, no pipelining).
+template <class F>
+chw_status host_stage(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch, uint64_t n, F&& fn) {
+  const size_t bytes = (size_t)batch * (size_t)n * elem_size(dtype);
+  if (bytes == 0) return fn(nullptr);
+  void* d = nullptr;
+  if (cudaMalloc(&d, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CHW_ERR_RESOURCE, "cannot allocate device buffer");
+  }
+  chw_status s = CHW_OK;
+  cudaError_t e = cudaMemcpy(d, in_host, bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpy");
+  if (s == CHW_OK) s = fn(d);
+  if (s == CHW_OK) {
+    e = cudaStreamSynchronize(nullptr);
+    if (e != cudaSuccess) s = cuda_fail(e, "cudaStreamSynchronize");
+  }
+  if (s == CHW_OK) {
+    e = cudaMemcpy(out_host, d, bytes, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpy");
+  }
+  cudaFree(d);
+  return s;
+}
+
+}  // namespace
+
 extern "C" {
 
 chw_status chw_b200_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
@@ -522,6 +552,24 @@ chw_status chw_b200_haar_walsh_forward(const void* in, void* out, chw_dtype dtyp
     CHW_CUDA(cudaMemcpy2DAsync(o + blk, n * es, tmp, blk, blk, (size_t)batch, cudaMemcpyDeviceToDevice, st));
   }
   return CHW_OK;
+}
+
+chw_status chw_b200_haar_inverse_host(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
+                                      uint64_t n, chw_mode mode) {
+  if (chw_status s = validate("haar_inverse", dtype, n, mode)) return s;
+  if (batch <= 0) return batch < 0 ? fail(CHW_ERR_ARGUMENT, "haar_inverse: negative batch") : CHW_OK;
+  return host_stage(in_host, out_host, dtype, batch, n, [&](void* d) {
+    return chw_b200_haar_inverse(d, d, dtype, batch, n, mode, nullptr, 0, nullptr);
+  });
+}
+
+chw_status chw_b200_haar_walsh_forward_host(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
+                                            uint64_t n, chw_mode mode) {
+  if (chw_status s = validate("haar_walsh_forward", dtype, n, mode)) return s;
+  if (batch <= 0) return batch < 0 ? fail(CHW_ERR_ARGUMENT, "haar_walsh_forward: negative batch") : CHW_OK;
+  return host_stage(in_host, out_host, dtype, batch, n, [&](void* d) {
+    return chw_b200_haar_walsh_forward(d, d, dtype, batch, n, mode, nullptr);
+  });
 }
 
 chw_status chw_b200_parallel_execute(void* x, chw_dtype dtype, uint64_t n, int workers,
