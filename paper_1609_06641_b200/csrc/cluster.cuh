@@ -20,7 +20,7 @@
 
 #include <cooperative_groups.h>
 
-#include "pipelined.cuh"
+#include "plans.cuh"
 
 namespace chwb {
 
@@ -158,61 +158,5 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 2)
 }
 
 
-// Pipelined variant: the next row's quarter is prefetched with 16-byte cp.async
-// into a shared-memory stage while the current row computes and exchanges
-// (one CTA per SM: 64 KiB stage + 64 KiB transpose/exchange buffer).
-template <bool SCALE>
-__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
-    cluster_m16_pipe_kernel(const float* __restrict__ in, float* __restrict__ out, uint64_t rows,
-                            float scale) {
-  using K = ClusterF32M16;
-  namespace cg = cooperative_groups;
-  extern __shared__ __align__(128) float smem_cl[];
-  float* stage = smem_cl;
-  float* buf = smem_cl + K::LOCAL;
-  cg::cluster_group cl = cg::this_cluster();
-  const uint32_t r = cl.block_rank();
-  const uint64_t cid = blockIdx.x / K::CLUSTER;
-  const uint64_t ncl = gridDim.x / K::CLUSTER;
-  const uint32_t tid = threadIdx.x;
-  const uint32_t w = tid >> 5;
-  const uint32_t lane = tid & 31u;
-  const uint32_t rp = (((w >> 1) & 1u) << 1) | ((w >> 2) & 1u);
-  float* gbuf = cl.map_shared_rank(buf, rp);
-  const uint32_t xbase = K::S2::apply((lane << 6) | ((w & 1u) << 11) | (r << 12));
-  float v[64];
-  uint64_t row = cid;
-  if (row < rows) issue_tile_copy<K::L0, IdMap, NoSwz>(stage, in + (row << K::M) + (uint64_t)r * K::LOCAL, tid);
-  cp_async_commit();
-  for (; row < rows; row += ncl) {
-    cp_async_wait<0>();
-    __syncthreads();  // stage landed; previous row's reads of buf are done
-    smem_load<K::L0, NoSwz>(stage, v, tid);
-    butterflies<K::L0, BL<0, 1, 10, 11, 12, 13>, false>(v);
-    smem_store<K::L0, K::S1>(buf, v, tid);
-    __syncthreads();  // stage consumed, buf complete
-    const uint64_t nrow = row + ncl;
-    if (nrow < rows)
-      issue_tile_copy<K::L0, IdMap, NoSwz>(stage, in + (nrow << K::M) + (uint64_t)r * K::LOCAL, tid);
-    cp_async_commit();
-    smem_load<K::L1, K::S1>(buf, v, tid);
-    butterflies<K::L1, BL<2, 3, 4, 5, 6, 7>, false>(v);
-    shfl_butterfly<K::L1, 8, false>(v, tid);
-    shfl_butterfly<K::L1, 9, false>(v, tid);
-    cluster_sync_relaxed();  // every CTA finished reading its buf
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const uint32_t a = xbase ^ (uint32_t)(q << 2);
-      *reinterpret_cast<float4*>(gbuf + a) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    }
-    cl.sync();  // exchange visible
-    smem_load<K::L2, K::S2>(buf, v, tid);
-    butterflies<K::L2, BL<12, 13>, false>(v);
-    store_global<K::L2, K::Rev14, SCALE, Cache::kStream>(out + (row << K::M) + (uint64_t)r * K::LOCAL, v, tid,
-                                                         scale);
-  }
-  cp_async_wait<0>();
-  cl.sync();
-}
 
 }  // namespace chwb

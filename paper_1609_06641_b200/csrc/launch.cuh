@@ -278,27 +278,6 @@ chw_status launch_cluster_m16(const float* in, float* out, int64_t batch, float 
     const char* e = std::getenv("CHW_B200_XCH");
     return e ? std::atoi(e) : 1;
   }();
-  if (xch == 3) {
-    using K = ClusterF32M16;
-    constexpr auto k = cluster_m16_pipe_kernel<SCALE>;
-    constexpr int smem = 2 * K::SMEM_BYTES;
-    if (chw_status s = prep_kernel<k>(smem)) return s;
-    static int ncl3[64] = {0};
-    int dev = 0;
-    if (chw_status s = current_device(&dev)) return s;
-    if (ncl3[dev] == 0) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(K::CLUSTER * 1024, 1, 1);
-      cfg.blockDim = dim3(K::NT, 1, 1);
-      cfg.dynamicSmemBytes = smem;
-      int ncl = 0;
-      CHW_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
-      ncl3[dev] = std::max(1, ncl);
-    }
-    const uint64_t clusters = std::min<uint64_t>((uint64_t)batch, (uint64_t)ncl3[dev]);
-    k<<<(unsigned)(clusters * K::CLUSTER), K::NT, smem, st>>>(in, out, (uint64_t)batch, scale);
-    return check_launch("cluster_m16_pipe_kernel");
-  }
   if (xch == 0) return launch_cluster_m16_x<SCALE, 0>(in, out, batch, scale, st);
   if (xch == 2) return launch_cluster_m16_x<SCALE, 2>(in, out, batch, scale, st);
   return launch_cluster_m16_x<SCALE, 1>(in, out, batch, scale, st);
