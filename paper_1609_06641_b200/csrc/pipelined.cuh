@@ -314,4 +314,54 @@ __global__ void __launch_bounds__(F::NT, FusedPipe<F>::MIN_BLOCKS)
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// K4P: one statically scheduled pipelined pass over independent tiles whose
+// source/destination offsets come from a geometry functor (phase A or B of a
+// two-pass schedule; no cross-CTA dependencies inside a launch).
+// ---------------------------------------------------------------------------
+template <class Item, class Geo, bool SCALE, int STAGES, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    pass_p_kernel(const float* __restrict__ src, float* __restrict__ dst, uint64_t nitems, float scale) {
+  constexpr int TILE = Item::TILE;
+  extern __shared__ __align__(128) float smem_pp[];
+  float* stages = smem_pp;
+  float* work = smem_pp + STAGES * TILE;
+  const uint32_t tid = threadIdx.x;
+  const uint64_t stride = gridDim.x;
+  uint64_t item = blockIdx.x;
+#pragma unroll
+  for (int s = 0; s < STAGES; ++s) {
+    const uint64_t it = item + (uint64_t)s * stride;
+    if (it < nitems) Item::copy(stages + s * TILE, src + Geo::src_off(it), tid);
+    cp_async_commit();
+  }
+  float v[Item::E];
+  for (uint32_t k = 0; item < nitems; ++k, item += stride) {
+    const int s = k % STAGES;
+    cp_async_wait<STAGES - 1>();
+    __syncthreads();
+    Item::phase0(stages + s * TILE, work, v, tid);
+    __syncthreads();
+    const uint64_t nxt = item + (uint64_t)STAGES * stride;
+    if (nxt < nitems) Item::copy(stages + s * TILE, src + Geo::src_off(nxt), tid);
+    cp_async_commit();
+    Item::template phase1<SCALE>(work, dst + Geo::dst_off(item), v, tid, scale);
+  }
+  cp_async_wait<0>();
+}
+
+// Geometry of the m = 24 two-pass schedule (tiles of FusedF32M24).
+struct GeoA24 {
+  __device__ __forceinline__ static uint64_t src_off(uint64_t it) { return it << 14; }
+  __device__ __forceinline__ static uint64_t dst_off(uint64_t it) { return it << 14; }
+};
+struct GeoB24 {
+  __device__ __forceinline__ static uint64_t src_off(uint64_t it) {
+    return ((it >> 10) << 24) | deposit<FusedF32M24::B::OuterAddr>((uint32_t)(it & 1023u));
+  }
+  __device__ __forceinline__ static uint64_t dst_off(uint64_t it) {
+    return ((it >> 10) << 24) | deposit<FusedF32M24::B::OuterOut>((uint32_t)(it & 1023u));
+  }
+};
+
 }  // namespace chwb

@@ -98,7 +98,7 @@ def test_plan_selection():
     assert chw.plan_name(chw.DTYPE_F32, 4096) == "k1-tuned"
     assert chw.plan_name(chw.DTYPE_BF16, 128) == "k1-tuned"
     assert chw.plan_name(chw.DTYPE_F64, 1024).startswith("k1")
-    assert chw.plan_name(chw.DTYPE_F32, 1 << 24) == "k5-fused-2phase"
+    assert chw.plan_name(chw.DTYPE_F32, 1 << 24) == "k4p-two-pass-pipelined"
     assert chw.plan_name(chw.DTYPE_F32, 1 << 16) == "k3-cluster-dsmem"
     assert chw.plan_name(chw.DTYPE_F32, 1 << 20).startswith("k4-multipass")
 
