@@ -80,7 +80,9 @@ typedef enum chw_order { CHW_ORDER_DYADIC = 0, CHW_ORDER_NATURAL = 1, CHW_ORDER_
  * batch*n contiguous elements of `dtype` (in == out is allowed: in place).
  * `workspace` may be NULL (the library allocates and caches one per device) or
  * a device buffer of at least chw_b200_workspace_bytes(dtype, batch, n) bytes.
- * `stream` is a cudaStream_t (NULL = legacy default stream).  Asynchronous. */
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Asynchronous.
+ * Device buffers (in, out, workspace) must be 16-byte aligned, as cudaMalloc
+ * and torch allocations are (the kernels move 16-byte vectors and TMA tiles). */
 chw_status chw_b200_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
                             chw_mode mode, void* workspace, size_t workspace_bytes, void* stream);
 

@@ -3,6 +3,7 @@
 // compiled in their own translation unit so the build parallelises.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,6 +19,7 @@
 #include "pipelined.cuh"
 #include "warpspec.cuh"
 #include "cluster.cuh"
+#include "rowpipe.cuh"
 
 namespace chwb {
 
@@ -283,12 +285,102 @@ chw_status launch_cluster_m16(const float* in, float* out, int64_t batch, float 
   return launch_cluster_m16_x<SCALE, 1>(in, out, batch, scale, st);
 }
 
-inline bool cluster_enabled() {
-  static const bool on = [] {
+// f32 m = 16 schedule: 'c' K3 cluster/DSMEM, 'f' K5 fused dataflow, 'r<v>' K6
+// per-CTA row pipeline (rowpipe.cuh) variant v (stages x CTAs/SM, below).
+inline char m16_mode() {
+  static const char mode = [] {
     const char* e = std::getenv("CHW_B200_M16");
-    return !(e && e[0] == 'f');
+    return (e && (e[0] == 'f' || e[0] == 'r' || e[0] == 'c')) ? e[0] : 'r';
   }();
-  return on;
+  return mode;
+}
+inline bool cluster_enabled() { return m16_mode() == 'c'; }
+inline int rowpipe_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("CHW_B200_M16");
+    return (e && e[0] == 'r' && e[1] >= '1' && e[1] <= '4') ? e[1] - '0' : 1;
+  }();
+  return v;
+}
+
+// K6 workspace: one row per CTA (one CTA per SM).
+inline size_t rowpipe_workspace(int64_t batch) {
+  if (batch <= 0) return 0;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(batch, (int64_t)sms);
+  return (size_t)grid * ((size_t)1 << RowPipeF32M16<0>::M) * sizeof(float);
+}
+
+// Tensor maps over a K6 workspace of `ctas` rows (tile order in smem):
+//   layout 0 column tile: [ctas*256][16][16] floats (W bits 8..15 + CTA, 4..7, 0..3), box {16, 1, 256};
+//   layout 1 region tile: [ctas*16][W bits 4..7][W bits 8..11][W bits 0..3], box {16, 16, 16, 1}.
+using TmapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline chw_status tmap_encoder(TmapEncodeFn* out) {
+  static TmapEncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CHW_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess)
+      return fail(CHW_ERR_CUDA, "chw_forward: cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<TmapEncodeFn>(p);
+  }
+  *out = fn;
+  return CHW_OK;
+}
+inline chw_status rowpipe_tmaps(void* ws, int ctas, TmapParam* t0, TmapParam* t1) {
+  static_assert(sizeof(CUtensorMap) == sizeof(TmapParam), "tensor map size");
+  TmapEncodeFn fn = nullptr;
+  if (chw_status s = tmap_encoder(&fn)) return s;
+  const cuuint64_t d0[3] = {16, 16, (cuuint64_t)ctas * 256};
+  const cuuint64_t s0[2] = {64, 1024};
+  const cuuint32_t b0[3] = {16, 1, 256};
+  const cuuint32_t e[4] = {1, 1, 1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(t0), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ws, d0, s0, b0, e,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CHW_ERR_CUDA, "chw_forward: cuTensorMapEncodeTiled (layout 0) failed");
+  const cuuint64_t d1[4] = {16, 16, 16, (cuuint64_t)ctas * 16};
+  const cuuint64_t s1[3] = {1024, 64, 16384};
+  const cuuint32_t b1[4] = {16, 16, 16, 1};
+  r = fn(reinterpret_cast<CUtensorMap*>(t1), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ws, d1, s1, b1, e,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CHW_ERR_CUDA, "chw_forward: cuTensorMapEncodeTiled (layout 1) failed");
+  return CHW_OK;
+}
+
+template <bool SCALE, int SA, int SB, int HINT>
+chw_status launch_rowpipe_ws_m16_x(const float* in, float* out, void* ws, int64_t batch, float scale,
+                                   cudaStream_t st) {
+  using P = RowPipeF32M16<HINT>;
+  constexpr auto k = rowpipe_ws_kernel<P, SA, SB, SCALE>;
+  if (((uintptr_t)in | (uintptr_t)out | (uintptr_t)ws) & 15u)
+    return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers and workspace must be 16-byte aligned");
+  constexpr int smem = (SA + SB + 4) * P::TILE * 4;
+  if (chw_status s = prep_kernel<k>(smem)) return s;
+  int dev = 0, sms = 0;
+  if (chw_status s = current_device(&dev)) return s;
+  CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = (int)std::min<int64_t>(batch, (int64_t)sms);
+  TmapParam t0, t1;
+  if (chw_status s = rowpipe_tmaps(ws, grid, &t0, &t1)) return s;
+  k<<<grid, 2 * P::NT + 64, smem, st>>>(in, out, static_cast<float*>(ws), (uint64_t)batch, scale, t0, t1);
+  return check_launch("rowpipe_ws_kernel");
+}
+// Variants (measured): ring depths (A, B) and L2 hints.
+template <bool SCALE>
+chw_status launch_rowpipe_m16(const float* in, float* out, void* ws, int64_t batch, float scale,
+                              cudaStream_t st) {
+  switch (rowpipe_variant()) {
+    case 2: return launch_rowpipe_ws_m16_x<SCALE, 6, 4, 3>(in, out, ws, batch, scale, st);
+    case 3: return launch_rowpipe_ws_m16_x<SCALE, 5, 5, 1>(in, out, ws, batch, scale, st);
+    case 4: return launch_rowpipe_ws_m16_x<SCALE, 7, 3, 1>(in, out, ws, batch, scale, st);
+    default: return launch_rowpipe_ws_m16_x<SCALE, 6, 4, 1>(in, out, ws, batch, scale, st);
+  }
 }
 
 // Two-pass static pipelined schedule for f32 m = 24 (BASELINE cfg5): rows in
@@ -347,6 +439,7 @@ size_t k4_workspace_m(int m, int64_t batch, size_t inter) {
     using F = typename FusedSelect<T, MLO>::F;
     if constexpr (!std::is_void<F>::value) {
       size_t w = FusedPlanGeom<F>::workspace(batch);
+      if constexpr (std::is_same<T, float>::value && MLO == 16) w = std::max(w, rowpipe_workspace(batch));
       if constexpr (std::is_same<T, float>::value && MLO == 24)
         w = std::max(w, (size_t)std::min<int64_t>(batch, kM24Chunk) << 26);  // two-pass intermediate
       return w;
@@ -364,6 +457,7 @@ chw_status launch_m(const T* in, T* out, void* ws, int64_t batch, typename IoTra
   } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {
     if constexpr (std::is_same<T, float>::value && M == 16) {
       if (cluster_enabled()) return launch_cluster_m16<SC == Scaling::kDeferred>(in, out, batch, scale, st);
+      if (m16_mode() == 'r') return launch_rowpipe_m16<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
     }
     if constexpr (std::is_same<T, float>::value && M == 24) {
       if (const char* e = std::getenv("CHW_B200_M24"); !(e && e[0] == 'f'))
@@ -396,7 +490,7 @@ const char* plan_name_m(int m) {
     if constexpr (M <= Regime<T>::K1MAX) {
       return K1Select<T, M>::kTuned ? "k1-tuned" : "k1-generic";
     } else if constexpr (std::is_same<T, float>::value && M == 16) {
-      return "k3-cluster-dsmem";
+      return m16_mode() == 'c' ? "k3-cluster-dsmem" : m16_mode() == 'r' ? "k6-rowpipe" : "k5-fused-2phase";
     } else if constexpr (std::is_same<T, float>::value && M == 24) {
       return "k4p-two-pass-pipelined";
     } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {

@@ -169,6 +169,10 @@ PLANS = [
          [Layout([0, 1, 2, 6], [3, 4, 5, 7, 8, 9, 10, 11]), Layout([3, 4, 5, 6], [0, 1, 2, 7, 8, 9, 10, 11])],
          [[0, 1, 2, 6], [3, 4, 5]], swz=[(5, 2), (7, 3), (8, 4)], out_pos=rev_pos(7), io_bytes=2,
          need=range(7)),
+    Plan("f32 m=16 K6 B tile (RowPipeF32M16 ItemB0)", 12,
+         [Layout([0, 1, 5, 8, 9], [2, 3, 4, 6, 7, 10, 11]), Layout([4, 6, 7, 10, 11], [9, 8, 5, 0, 1, 2, 3])],
+         [[5, 8, 9], [4, 6, 7, 10, 11]], swz=[(5, 2), (8, 3), (9, 4)],
+         out_pos=lambda b: [13, 12, 15, 14, 7, 6, 5, 4, 3, 2, 1, 0][b], need=range(4, 12)),
 ]
 
 
