@@ -298,7 +298,7 @@ inline bool cluster_enabled() { return m16_mode() == 'c'; }
 inline int rowpipe_variant() {
   static const int v = [] {
     const char* e = std::getenv("CHW_B200_M16");
-    return (e && e[0] == 'r' && e[1] >= '1' && e[1] <= '4') ? e[1] - '0' : 1;
+    return (e && e[0] == 'r' && e[1] >= '1' && e[1] <= '7') ? e[1] - '0' : 6;  // default: K6f (4, 6)
   }();
   return v;
 }
@@ -371,7 +371,28 @@ chw_status launch_rowpipe_ws_m16_x(const float* in, float* out, void* ws, int64_
   k<<<grid, 2 * P::NT + 64, smem, st>>>(in, out, static_cast<float*>(ws), (uint64_t)batch, scale, t0, t1);
   return check_launch("rowpipe_ws_kernel");
 }
-// Variants (measured): ring depths (A, B) and L2 hints.
+template <bool SCALE, int SA, int SB, int HINT>
+chw_status launch_rowpipe_ws4_m16_x(const float* in, float* out, void* ws, int64_t batch, float scale,
+                                    cudaStream_t st) {
+  using P = RowPipeF32M16<HINT>;
+  constexpr auto k = rowpipe_ws4_kernel<P, SA, SB, SCALE>;
+  if (((uintptr_t)in | (uintptr_t)out | (uintptr_t)ws) & 15u)
+    return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers and workspace must be 16-byte aligned");
+  constexpr int smem = (SA + SB + 4) * P::TILE * 4;
+  if (chw_status s = prep_kernel<k>(smem)) return s;
+  int dev = 0, sms = 0;
+  if (chw_status s = current_device(&dev)) return s;
+  CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = (int)std::min<int64_t>(batch, (int64_t)sms);
+  TmapParam t0, t1;
+  if (chw_status s = rowpipe_tmaps(ws, grid, &t0, &t1)) return s;
+  k<<<grid, 4 * P::NT + 64, smem, st>>>(in, out, static_cast<float*>(ws), (uint64_t)batch, scale, t0, t1);
+  return check_launch("rowpipe_ws4_kernel");
+}
+
+// Variants (measured): K6e (one compute group per stream)
+// r1..r4 with ring depths (A, B) and L2 hints; K6f (two groups per stream,
+// even ring depths) r5..r7.  Default r6.
 template <bool SCALE>
 chw_status launch_rowpipe_m16(const float* in, float* out, void* ws, int64_t batch, float scale,
                               cudaStream_t st) {
@@ -379,6 +400,9 @@ chw_status launch_rowpipe_m16(const float* in, float* out, void* ws, int64_t bat
     case 2: return launch_rowpipe_ws_m16_x<SCALE, 6, 4, 3>(in, out, ws, batch, scale, st);
     case 3: return launch_rowpipe_ws_m16_x<SCALE, 5, 5, 1>(in, out, ws, batch, scale, st);
     case 4: return launch_rowpipe_ws_m16_x<SCALE, 7, 3, 1>(in, out, ws, batch, scale, st);
+    case 5: return launch_rowpipe_ws4_m16_x<SCALE, 6, 4, 1>(in, out, ws, batch, scale, st);
+    case 6: return launch_rowpipe_ws4_m16_x<SCALE, 4, 6, 1>(in, out, ws, batch, scale, st);
+    case 7: return launch_rowpipe_ws4_m16_x<SCALE, 8, 2, 1>(in, out, ws, batch, scale, st);
     default: return launch_rowpipe_ws_m16_x<SCALE, 6, 4, 1>(in, out, ws, batch, scale, st);
   }
 }

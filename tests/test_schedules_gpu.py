@@ -1,7 +1,7 @@
 """GPU parity of every selectable schedule of the long-row paths, one
 subprocess per variant (the library reads CHW_B200_* once per process).
 
-m = 16 (cfg4): K6 row pipeline variants r1..r4 (default r1), the K3 cluster
+m = 16 (cfg4): K6 row pipeline variants r1..r7 (default r6), the K3 cluster
 kernel (c) and the K5 fused dataflow kernel (f); m = 24 (cfg5): the default
 two-pass schedule and the fused one (f).  Each run checks f32 Orthonormal
 against the oracle (rel-L2 <= 1e-5), in-place == out-of-place, the exact
@@ -30,7 +30,7 @@ def _run(env_extra, m, rows):
     return p.stdout
 
 
-@pytest.mark.parametrize("variant", ["r1", "r2", "r3", "r4", "c", "f"])
+@pytest.mark.parametrize("variant", ["r1", "r2", "r3", "r4", "r5", "r6", "r7", "c", "f"])
 def test_m16_schedules(cuda, variant):
     out = _run({"CHW_B200_M16": variant}, 16, [1, 2, 3, 149, 300, 445])
     want = {"r": "k6-rowpipe", "c": "k3-cluster-dsmem", "f": "k5-fused-2phase"}[variant[0]]
