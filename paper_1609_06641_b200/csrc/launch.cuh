@@ -20,6 +20,8 @@
 #include "warpspec.cuh"
 #include "cluster.cuh"
 #include "rowpipe.cuh"
+#include "k1t.cuh"
+#include "passtma.cuh"
 
 namespace chwb {
 
@@ -90,11 +92,67 @@ chw_status launch_k1p(const float* in, float* out, int64_t batch, float scale, c
   return check_launch("k1p_kernel");
 }
 
+// K1T (k1t.cuh): TMA-fed single-pass kernel for f32 m = 12 (cfg2, default).
+// CHW_B200_K1T=0 selects K1P, 1..4 the (stages, groups) variants below.
+// Same-box A/B: variant 2 95.3-95.9 % vs K1P 90.7-91.2 %.
+inline int k1t_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("CHW_B200_K1T");
+    return (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 2;
+  }();
+  return v;
+}
+template <class Item, int TB, int S, int NG, bool SCALE>
+chw_status launch_k1t_x(const typename Item::IO* in, typename Item::IO* out, int64_t tiles, float scale,
+                        cudaStream_t st) {
+  constexpr auto k = k1t_kernel<Item, TB, S, NG, SCALE>;
+  constexpr int smem = S * Item::TILE * (int)sizeof(typename Item::IO) + NG * Item::TILE * 4;
+  if (((uintptr_t)in | (uintptr_t)out) & 15u)
+    return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers must be 16-byte aligned");
+  if (chw_status s = prep_kernel<k>(smem)) return s;
+  int dev = 0, sms = 0;
+  if (chw_status s = current_device(&dev)) return s;
+  CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms);
+  k<<<grid, NG * Item::L0::NT + 32, smem, st>>>(in, out, (uint64_t)tiles, scale);
+  return check_launch("k1t_kernel");
+}
+template <bool SCALE>
+chw_status launch_k1t(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
+  switch (k1t_variant()) {
+    case 1: return launch_k1t_x<ItemF32M12, 12, 8, 4, SCALE>(in, out, batch, scale, st);
+    case 3: return launch_k1t_x<ItemF32M12, 12, 9, 3, SCALE>(in, out, batch, scale, st);
+    case 4: return launch_k1t_x<ItemF32M12, 12, 10, 2, SCALE>(in, out, batch, scale, st);
+    default: return launch_k1t_x<ItemF32M12, 12, 8, 2, SCALE>(in, out, batch, scale, st);
+  }
+}
+// bf16 m = 7 (cfg3): CHW_B200_K1T_BF16=1..3 selects the TMA-fed kernel
+// (tiles of 32 rows; the batch remainder goes through the K1 kernel).  Off by
+// default: same-box A/B 84.7-87.8 % (variant 2) vs K1 84.9-85.2 %, the 256-
+// thread bf16 item allows at most 3 groups per CTA.
+inline int k1t_bf16_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("CHW_B200_K1T_BF16");
+    return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
+  }();
+  return v;
+}
+template <bool SCALE>
+chw_status launch_k1t_bf16(const __nv_bfloat16* in, __nv_bfloat16* out, int64_t tiles, float scale,
+                           cudaStream_t st) {
+  switch (k1t_bf16_variant()) {
+    case 2: return launch_k1t_x<ItemBF16M7, 12, 12, 3, SCALE>(in, out, tiles, scale, st);
+    case 3: return launch_k1t_x<ItemBF16M7, 12, 8, 2, SCALE>(in, out, tiles, scale, st);
+    default: return launch_k1t_x<ItemBF16M7, 12, 16, 2, SCALE>(in, out, tiles, scale, st);
+  }
+}
+
 // Output-order variants of a plan are produced by swapping the output map.
 template <class T, int M, Scaling SC>
 chw_status launch_k1(const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale,
                      cudaStream_t st) {
   if constexpr (std::is_same<T, float>::value && M == 12) {
+    if (k1t_variant() > 0) return launch_k1t<SC == Scaling::kDeferred>(in, out, batch, scale, st);
     if (pipeline_enabled())
       return launch_k1p<PipeF32M12, SC == Scaling::kDeferred>(in, out, batch, scale, st);
   }
@@ -103,7 +161,14 @@ chw_status launch_k1(const T* in, T* out, int64_t batch, typename IoTraits<T>::C
   constexpr int ROWS_PER_TILE = 1 << (TB - M);
   const uint64_t full = (uint64_t)batch / ROWS_PER_TILE;
   const uint64_t tail_rows = (uint64_t)batch % ROWS_PER_TILE;
-  if (full > 0) {
+  bool full_done = false;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value && M == 7) {
+    if (full > 0 && k1t_bf16_variant() > 0) {
+      if (chw_status s = launch_k1t_bf16<SC == Scaling::kDeferred>(in, out, (int64_t)full, scale, st)) return s;
+      full_done = true;
+    }
+  }
+  if (full > 0 && !full_done) {
     constexpr auto k = k1_kernel<Plan, SC, false>;
     if (chw_status s = prep_kernel<k>(Plan::SMEM_BYTES)) return s;
     for (uint64_t t0 = 0; t0 < full; t0 += 0x7fffffffull) {
@@ -440,6 +505,52 @@ chw_status launch_two_pass_m24(const float* in, float* out, void* ws, int64_t ba
   return CHW_OK;
 }
 
+// K4T (passtma.cuh): the same two-pass schedule fed by TMA, in-place tile
+// transposes (3 tiles in flight per SM).  CHW_B200_M24=t.
+inline chw_status m24_mid_tmap(float* mid, int64_t rows, TmapParam* t) {
+  TmapEncodeFn fn = nullptr;
+  if (chw_status s = tmap_encoder(&fn)) return s;
+  const cuuint64_t dims[5] = {8, 1024, 256, 8, (cuuint64_t)rows};
+  const cuuint64_t strides[4] = {32, 32768, 8388608, 67108864};
+  const cuuint32_t box[5] = {8, 1, 256, 8, 1};
+  const cuuint32_t e[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(t), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, mid, dims, strides, box, e,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CHW_ERR_CUDA, "chw_forward: cuTensorMapEncodeTiled (m = 24) failed");
+  return CHW_OK;
+}
+template <bool SCALE>
+chw_status launch_two_pass_tma_m24(const float* in, float* out, void* ws, int64_t batch, float scale,
+                                   cudaStream_t st) {
+  using P = PassTmaF32M24;
+  constexpr int S = 3;
+  constexpr int smem = S * P::TILE * 4;
+  constexpr auto ka = pass_tma_kernel<P::ItemA, GeoA24, false, S, false>;
+  constexpr auto kb = pass_tma_kernel<P::ItemB, GeoB24, true, S, SCALE>;
+  if (((uintptr_t)in | (uintptr_t)out | (uintptr_t)ws) & 15u)
+    return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers and workspace must be 16-byte aligned");
+  if (chw_status s = prep_kernel<ka>(smem)) return s;
+  if (chw_status s = prep_kernel<kb>(smem)) return s;
+  int dev = 0, sms = 0;
+  if (chw_status s = current_device(&dev)) return s;
+  CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  float* mid = static_cast<float*>(ws);
+  TmapParam none{};
+  for (int64_t r0 = 0; r0 < batch; r0 += kM24Chunk) {
+    const int64_t rows = std::min<int64_t>(kM24Chunk, batch - r0);
+    const uint64_t items = (uint64_t)rows * 1024;
+    const unsigned grid = (unsigned)std::min<uint64_t>(items, (uint64_t)sms);
+    ka<<<grid, P::NT + 32, smem, st>>>(in + ((uint64_t)r0 << 24), mid, items, scale, none);
+    if (chw_status s = check_launch("pass_tma_kernel(A)")) return s;
+    TmapParam tm;
+    if (chw_status s = m24_mid_tmap(mid, rows, &tm)) return s;
+    kb<<<grid, P::NT + 32, smem, st>>>(mid, out + ((uint64_t)r0 << 24), items, scale, tm);
+    if (chw_status s = check_launch("pass_tma_kernel(B)")) return s;
+  }
+  return CHW_OK;
+}
+
 // Fused spec per (T, M), void when none exists (the K4 multi-pass path is used).
 template <class T, int M>
 struct FusedSelect {
@@ -484,6 +595,8 @@ chw_status launch_m(const T* in, T* out, void* ws, int64_t batch, typename IoTra
       if (m16_mode() == 'r') return launch_rowpipe_m16<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
     }
     if constexpr (std::is_same<T, float>::value && M == 24) {
+      if (const char* e = std::getenv("CHW_B200_M24"); e && e[0] == 't')
+        return launch_two_pass_tma_m24<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
       if (const char* e = std::getenv("CHW_B200_M24"); !(e && e[0] == 'f'))
         return launch_two_pass_m24<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
     }
@@ -512,6 +625,10 @@ const char* plan_name_m(int m) {
   } else {
     if (m != M) return plan_name_m<T, M + 1>(m);
     if constexpr (M <= Regime<T>::K1MAX) {
+      if constexpr (std::is_same<T, float>::value && M == 12)
+        if (k1t_variant() > 0) return "k1t-tma";
+      if constexpr (std::is_same<T, __nv_bfloat16>::value && M == 7)
+        if (k1t_bf16_variant() > 0) return "k1t-tma";
       return K1Select<T, M>::kTuned ? "k1-tuned" : "k1-generic";
     } else if constexpr (std::is_same<T, float>::value && M == 16) {
       return m16_mode() == 'c' ? "k3-cluster-dsmem" : m16_mode() == 'r' ? "k6-rowpipe" : "k5-fused-2phase";

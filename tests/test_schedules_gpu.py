@@ -49,3 +49,21 @@ def test_m16_default_is_rowpipe(cuda):
 def test_m24_schedules(cuda, variant):
     env = {} if variant == "default" else {"CHW_B200_M24": variant}
     _run(env, 24, [1, 3])
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
+def test_m12_k1t_variants(cuda, variant):
+    """f32 m = 12 (cfg2): K1T variants (TMA-fed, default 1) and K1P (0)."""
+    out = _run({"CHW_B200_K1T": variant}, 12, [1, 5, 148, 149, 1000, 4097])
+    assert ("k1t-tma" in out) == (variant != "0")
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
+def test_m7_bf16_k1t_variants(cuda, variant):
+    """bf16 m = 7 (cfg3): K1 (0, default) and the TMA-fed K1T variants."""
+    env = dict(os.environ)
+    env["CHW_B200_K1T_BF16"] = variant
+    p = subprocess.run([sys.executable, os.path.join(REPO, "tools", "sched_check.py"), "--m", "7", "--dtype", "bf16",
+                        "--rows", "1", "31", "32", "33", "4737"], env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+    assert ("k1t-tma" in p.stdout) == (variant != "0")
