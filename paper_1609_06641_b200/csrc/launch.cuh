@@ -505,8 +505,17 @@ chw_status launch_two_pass_m24(const float* in, float* out, void* ws, int64_t ba
   return CHW_OK;
 }
 
-// K4T (passtma.cuh): the same two-pass schedule fed by TMA, in-place tile
-// transposes (3 tiles in flight per SM).  CHW_B200_M24=t.
+// f32 m = 24 schedule: 't' K4T (default), 'p' K4P, 'f' K5 fused dataflow.
+inline char m24_mode() {
+  static const char mode = [] {
+    const char* e = std::getenv("CHW_B200_M24");
+    return (e && (e[0] == 't' || e[0] == 'p' || e[0] == 'f')) ? e[0] : 't';
+  }();
+  return mode;
+}
+// K4T (passtma.cuh): the K4P two-pass schedule fed by TMA, in-place tile
+// transposes (3 tiles in flight per SM).  Same-box A/B: 42.8-42.9 % vs K4P
+// 37.9-38.0 % of HBM peak (profiles/r01_ab_k4t.txt).
 inline chw_status m24_mid_tmap(float* mid, int64_t rows, TmapParam* t) {
   TmapEncodeFn fn = nullptr;
   if (chw_status s = tmap_encoder(&fn)) return s;
@@ -595,10 +604,9 @@ chw_status launch_m(const T* in, T* out, void* ws, int64_t batch, typename IoTra
       if (m16_mode() == 'r') return launch_rowpipe_m16<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
     }
     if constexpr (std::is_same<T, float>::value && M == 24) {
-      if (const char* e = std::getenv("CHW_B200_M24"); e && e[0] == 't')
-        return launch_two_pass_tma_m24<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
-      if (const char* e = std::getenv("CHW_B200_M24"); !(e && e[0] == 'f'))
-        return launch_two_pass_m24<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
+      const char m24 = m24_mode();
+      if (m24 == 't') return launch_two_pass_tma_m24<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
+      if (m24 == 'p') return launch_two_pass_m24<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
     }
     return launch_fused<typename FusedSelect<T, M>::F, SC == Scaling::kDeferred>(in, out, ws, batch,
                                                                                  scale, st);
@@ -633,7 +641,7 @@ const char* plan_name_m(int m) {
     } else if constexpr (std::is_same<T, float>::value && M == 16) {
       return m16_mode() == 'c' ? "k3-cluster-dsmem" : m16_mode() == 'r' ? "k6-rowpipe" : "k5-fused-2phase";
     } else if constexpr (std::is_same<T, float>::value && M == 24) {
-      return "k4p-two-pass-pipelined";
+      return m24_mode() == 't' ? "k4t-two-pass-tma" : m24_mode() == 'p' ? "k4p-two-pass-pipelined" : "k5-fused-2phase";
     } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {
       return "k5-fused-2phase";
     } else {

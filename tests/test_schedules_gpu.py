@@ -2,8 +2,8 @@
 subprocess per variant (the library reads CHW_B200_* once per process).
 
 m = 16 (cfg4): K6 row pipeline variants r1..r7 (default r6), the K3 cluster
-kernel (c) and the K5 fused dataflow kernel (f); m = 24 (cfg5): the default
-two-pass schedule and the fused one (f).  Each run checks f32 Orthonormal
+kernel (c) and the K5 fused dataflow kernel (f); m = 24 (cfg5): the TMA two-pass
+schedule (t, default), K4P (p) and the fused one (f).  Each run checks f32 Orthonormal
 against the oracle (rel-L2 <= 1e-5), in-place == out-of-place, the exact
 dyadic order through the integer probe, and Parseval on every row, for batch
 sizes that leave some CTAs with 0, 1, 2 or 3 rows (tools/sched_check.py).
@@ -45,10 +45,17 @@ def test_m16_default_is_rowpipe(cuda):
     assert "k6-rowpipe" in p.stdout
 
 
-@pytest.mark.parametrize("variant", ["default", "f"])
+@pytest.mark.parametrize("variant", ["default", "t", "p", "f"])
 def test_m24_schedules(cuda, variant):
-    env = {} if variant == "default" else {"CHW_B200_M24": variant}
-    _run(env, 24, [1, 3])
+    env = {k: v for k, v in os.environ.items() if k != "CHW_B200_M24"}
+    if variant != "default":
+        env["CHW_B200_M24"] = variant
+    cmd = [sys.executable, os.path.join(REPO, "tools", "sched_check.py"), "--m", "24", "--rows", "1", "3", "17"]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+    want = {"default": "k4t-two-pass-tma", "t": "k4t-two-pass-tma", "p": "k4p-two-pass-pipelined",
+            "f": "k5-fused-2phase"}[variant]
+    assert want in p.stdout
 
 
 @pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
