@@ -170,6 +170,37 @@ size_t ordered_workspace(chw_dtype dtype, int64_t batch, int m, chw_order order)
 chw_status dyadic_impl(const void* in, void* out, chw_dtype dtype, int64_t batch, int m, chw_mode mode,
                        void* ws, cudaStream_t st);
 
+int k1max_of(chw_dtype dtype) {
+  switch (dtype) {
+    case CHW_F64: return Regime<double>::K1MAX;
+    case CHW_I64: return Regime<long long>::K1MAX;
+    case CHW_F32: return Regime<float>::K1MAX;
+    case CHW_BF16: return Regime<__nv_bfloat16>::K1MAX;
+  }
+  return -1;
+}
+
+chw_status natural_k1_impl(const void* in, void* out, chw_dtype dtype, int64_t batch, int m, chw_mode mode,
+                           cudaStream_t st) {
+  const bool ortho = (mode == CHW_ORTHONORMAL);
+  switch (dtype) {
+    case CHW_F64:
+      return forward_k1_natural<double>(m, ortho, static_cast<const double*>(in), static_cast<double*>(out),
+                                        batch, 1.0, st);
+    case CHW_I64:
+      return forward_k1_natural<long long>(m, false, static_cast<const long long*>(in),
+                                           static_cast<long long*>(out), batch, 1, st);
+    case CHW_F32:
+      return forward_k1_natural<float>(m, ortho, static_cast<const float*>(in), static_cast<float*>(out), batch,
+                                       (float)ortho_scale(m), st);
+    case CHW_BF16:
+      return forward_k1_natural<__nv_bfloat16>(m, ortho, static_cast<const __nv_bfloat16*>(in),
+                                               static_cast<__nv_bfloat16*>(out), batch, (float)ortho_scale(m),
+                                               st);
+  }
+  return fail(CHW_ERR_UNSUPPORTED, "chw_forward: unknown dtype");
+}
+
 chw_status forward_impl(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
                         chw_mode mode, chw_order order, void* workspace, size_t workspace_bytes,
                         cudaStream_t st) {
@@ -194,6 +225,8 @@ chw_status forward_impl(const void* in, void* out, chw_dtype dtype, int64_t batc
     }
   }
   if (order == CHW_ORDER_DYADIC) return dyadic_impl(in, out, dtype, batch, m, mode, ws, st);
+  // Natural order for single-pass sizes: the order is the kernel's store map.
+  if (order == CHW_ORDER_NATURAL && m <= k1max_of(dtype)) return natural_k1_impl(in, out, dtype, batch, m, mode, st);
   // Other orders: dyadic result into the workspace, then one coalesced gather.
   void* tmp = static_cast<char*>(ws) + align256(workspace_for(dtype, batch, m));
   if (chw_status s = dyadic_impl(in, tmp, dtype, batch, m, mode, ws, st)) return s;

@@ -133,7 +133,7 @@ chw_status launch_k1t(const float* in, float* out, int64_t batch, float scale, c
 inline int k1t_bf16_variant() {
   static const int v = [] {
     const char* e = std::getenv("CHW_B200_K1T_BF16");
-    return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
+    return (e && e[0] >= '0' && e[0] <= '5') ? e[0] - '0' : 0;
   }();
   return v;
 }
@@ -143,6 +143,8 @@ chw_status launch_k1t_bf16(const __nv_bfloat16* in, __nv_bfloat16* out, int64_t 
   switch (k1t_bf16_variant()) {
     case 2: return launch_k1t_x<ItemBF16M7, 12, 12, 3, SCALE>(in, out, tiles, scale, st);
     case 3: return launch_k1t_x<ItemBF16M7, 12, 8, 2, SCALE>(in, out, tiles, scale, st);
+    case 4: return launch_k1t_x<ItemBF16M7, 12, 6, 3, SCALE>(in, out, tiles, scale, st);
+    case 5: return launch_k1t_x<ItemBF16M7, 12, 15, 3, SCALE>(in, out, tiles, scale, st);
     default: return launch_k1t_x<ItemBF16M7, 12, 16, 2, SCALE>(in, out, tiles, scale, st);
   }
 }
@@ -187,6 +189,45 @@ chw_status launch_k1(const T* in, T* out, int64_t batch, typename IoTraits<T>::C
     }
   }
   return CHW_OK;
+}
+
+// Natural-order single pass (f2): the generic K1 plan with identity store map.
+template <class T, int M, Scaling SC>
+chw_status launch_k1_nat(const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale, cudaStream_t st) {
+  using R = Regime<T>;
+  constexpr int TB = M > R::TMIN ? M : R::TMIN;
+  using Plan = GenericTilePlan<T, M, TB, R::EB, IdMap>;
+  constexpr int ROWS_PER_TILE = 1 << (TB - M);
+  const uint64_t full = (uint64_t)batch / ROWS_PER_TILE;
+  const uint64_t tail_rows = (uint64_t)batch % ROWS_PER_TILE;
+  if (full > 0) {
+    constexpr auto k = k1_kernel<Plan, SC, false>;
+    if (chw_status s = prep_kernel<k>(Plan::SMEM_BYTES)) return s;
+    for (uint64_t t0 = 0; t0 < full; t0 += 0x7fffffffull) {
+      const unsigned g = (unsigned)std::min<uint64_t>(full - t0, 0x7fffffffull);
+      k<<<g, Plan::NT, Plan::SMEM_BYTES, st>>>(in, out, t0, scale, 0);
+      if (chw_status s = check_launch("k1_kernel(natural)")) return s;
+    }
+  }
+  if constexpr (TB > M) {
+    if (tail_rows > 0) {
+      constexpr auto k = k1_kernel<Plan, SC, true>;
+      if (chw_status s = prep_kernel<k>(Plan::SMEM_BYTES)) return s;
+      k<<<1, Plan::NT, Plan::SMEM_BYTES, st>>>(in, out, full, scale, (uint32_t)(tail_rows << M));
+      if (chw_status s = check_launch("k1_kernel(natural tail)")) return s;
+    }
+  }
+  return CHW_OK;
+}
+template <class T, Scaling SC, int M, int MHI>
+chw_status dispatch_range_nat(int m, const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale,
+                              cudaStream_t st) {
+  if constexpr (M > MHI) {
+    return fail(CHW_ERR_UNSUPPORTED, "chw_forward: unsupported length");
+  } else {
+    if (m == M) return launch_k1_nat<T, M, SC>(in, out, batch, scale, st);
+    return dispatch_range_nat<T, SC, M + 1, MHI>(m, in, out, batch, scale, st);
+  }
 }
 
 template <class T, int M, Scaling SC, int p>
@@ -659,6 +700,9 @@ template <class T>
 chw_status forward_k1(int m, bool scaled_mode, const T* in, T* out, int64_t batch,
                       typename IoTraits<T>::C scale, cudaStream_t st);
 template <class T>
+chw_status forward_k1_natural(int m, bool scaled_mode, const T* in, T* out, int64_t batch,
+                              typename IoTraits<T>::C scale, cudaStream_t st);
+template <class T>
 chw_status forward_k4(int m, bool scaled_mode, const T* in, T* out, void* ws, int64_t batch,
                       typename IoTraits<T>::C scale, cudaStream_t st);
 template <class T>
@@ -685,6 +729,16 @@ struct ModeScaling {
     }                                                                                           \
     return dispatch_range<T, Scaling::kNone, 0, Regime<T>::K1MAX>(m, in, out, nullptr, batch,    \
                                                                    scale, st);                   \
+  }                                                                                             \
+  template <>                                                                                  \
+  chw_status forward_k1_natural<T>(int m, bool scaled_mode, const T* in, T* out, int64_t batch, \
+                                   typename IoTraits<T>::C scale, cudaStream_t st) {            \
+    if constexpr (!std::is_same<T, long long>::value) {                                         \
+      if (scaled_mode)                                                                          \
+        return dispatch_range_nat<T, ModeScaling<T>::kOrtho, 0, Regime<T>::K1MAX>(m, in, out,   \
+                                                                                  batch, scale, st); \
+    }                                                                                           \
+    return dispatch_range_nat<T, Scaling::kNone, 0, Regime<T>::K1MAX>(m, in, out, batch, scale, st); \
   }
 
 #define CHW_INSTANTIATE_K4(T)                                                                  \

@@ -171,10 +171,12 @@ struct TilePass {
   }
 };
 
-// Whole rows per tile (K1 generic): 2^(TB-M) rows of 2^M elements.
-template <class T, int M, int TB, int EB>
-struct GenericTilePlan : TilePass<T, T, IdMap, RevMap<M>, TB, EB, 0, M> {
-  using Base = TilePass<T, T, IdMap, RevMap<M>, TB, EB, 0, M>;
+// Whole rows per tile (K1 generic): 2^(TB-M) rows of 2^M elements.  MapOut
+// RevMap<M> stores dyadic order; IdMap stores natural order (SURVEY §8 f2:
+// the order folded into the store addresses, no extra pass).
+template <class T, int M, int TB, int EB, class MapOut = RevMap<M>>
+struct GenericTilePlan : TilePass<T, T, IdMap, MapOut, TB, EB, 0, M> {
+  using Base = TilePass<T, T, IdMap, MapOut, TB, EB, 0, M>;
   using IO = T;
   static constexpr int kM = M;
   template <bool PRED, Scaling SC>
