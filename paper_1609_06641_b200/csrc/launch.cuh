@@ -149,6 +149,45 @@ chw_status launch_k1t_bf16(const __nv_bfloat16* in, __nv_bfloat16* out, int64_t 
   }
 }
 
+// Natural-order single pass (f2): the generic K1 plan with identity store map.
+template <class T, int M, Scaling SC, class MapOut = IdMap>
+chw_status launch_k1_nat(const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale, cudaStream_t st) {
+  using R = Regime<T>;
+  constexpr int TB = M > R::TMIN ? M : R::TMIN;
+  using Plan = GenericTilePlan<T, M, TB, R::EB, MapOut>;
+  constexpr int ROWS_PER_TILE = 1 << (TB - M);
+  const uint64_t full = (uint64_t)batch / ROWS_PER_TILE;
+  const uint64_t tail_rows = (uint64_t)batch % ROWS_PER_TILE;
+  if (full > 0) {
+    constexpr auto k = k1_kernel<Plan, SC, false>;
+    if (chw_status s = prep_kernel<k>(Plan::SMEM_BYTES)) return s;
+    for (uint64_t t0 = 0; t0 < full; t0 += 0x7fffffffull) {
+      const unsigned g = (unsigned)std::min<uint64_t>(full - t0, 0x7fffffffull);
+      k<<<g, Plan::NT, Plan::SMEM_BYTES, st>>>(in, out, t0, scale, 0);
+      if (chw_status s = check_launch("k1_kernel(natural)")) return s;
+    }
+  }
+  if constexpr (TB > M) {
+    if (tail_rows > 0) {
+      constexpr auto k = k1_kernel<Plan, SC, true>;
+      if (chw_status s = prep_kernel<k>(Plan::SMEM_BYTES)) return s;
+      k<<<1, Plan::NT, Plan::SMEM_BYTES, st>>>(in, out, full, scale, (uint32_t)(tail_rows << M));
+      if (chw_status s = check_launch("k1_kernel(natural tail)")) return s;
+    }
+  }
+  return CHW_OK;
+}
+template <class T, Scaling SC, int M, int MHI>
+chw_status dispatch_range_nat(int m, const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale,
+                              cudaStream_t st) {
+  if constexpr (M > MHI) {
+    return fail(CHW_ERR_UNSUPPORTED, "chw_forward: unsupported length");
+  } else {
+    if (m == M) return launch_k1_nat<T, M, SC>(in, out, batch, scale, st);
+    return dispatch_range_nat<T, SC, M + 1, MHI>(m, in, out, batch, scale, st);
+  }
+}
+
 // Output-order variants of a plan are produced by swapping the output map.
 template <class T, int M, Scaling SC>
 chw_status launch_k1(const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale,
@@ -189,45 +228,6 @@ chw_status launch_k1(const T* in, T* out, int64_t batch, typename IoTraits<T>::C
     }
   }
   return CHW_OK;
-}
-
-// Natural-order single pass (f2): the generic K1 plan with identity store map.
-template <class T, int M, Scaling SC>
-chw_status launch_k1_nat(const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale, cudaStream_t st) {
-  using R = Regime<T>;
-  constexpr int TB = M > R::TMIN ? M : R::TMIN;
-  using Plan = GenericTilePlan<T, M, TB, R::EB, IdMap>;
-  constexpr int ROWS_PER_TILE = 1 << (TB - M);
-  const uint64_t full = (uint64_t)batch / ROWS_PER_TILE;
-  const uint64_t tail_rows = (uint64_t)batch % ROWS_PER_TILE;
-  if (full > 0) {
-    constexpr auto k = k1_kernel<Plan, SC, false>;
-    if (chw_status s = prep_kernel<k>(Plan::SMEM_BYTES)) return s;
-    for (uint64_t t0 = 0; t0 < full; t0 += 0x7fffffffull) {
-      const unsigned g = (unsigned)std::min<uint64_t>(full - t0, 0x7fffffffull);
-      k<<<g, Plan::NT, Plan::SMEM_BYTES, st>>>(in, out, t0, scale, 0);
-      if (chw_status s = check_launch("k1_kernel(natural)")) return s;
-    }
-  }
-  if constexpr (TB > M) {
-    if (tail_rows > 0) {
-      constexpr auto k = k1_kernel<Plan, SC, true>;
-      if (chw_status s = prep_kernel<k>(Plan::SMEM_BYTES)) return s;
-      k<<<1, Plan::NT, Plan::SMEM_BYTES, st>>>(in, out, full, scale, (uint32_t)(tail_rows << M));
-      if (chw_status s = check_launch("k1_kernel(natural tail)")) return s;
-    }
-  }
-  return CHW_OK;
-}
-template <class T, Scaling SC, int M, int MHI>
-chw_status dispatch_range_nat(int m, const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale,
-                              cudaStream_t st) {
-  if constexpr (M > MHI) {
-    return fail(CHW_ERR_UNSUPPORTED, "chw_forward: unsupported length");
-  } else {
-    if (m == M) return launch_k1_nat<T, M, SC>(in, out, batch, scale, st);
-    return dispatch_range_nat<T, SC, M + 1, MHI>(m, in, out, batch, scale, st);
-  }
 }
 
 template <class T, int M, Scaling SC, int p>
