@@ -118,4 +118,5 @@ __global__ void __launch_bounds__(NG * Item::L0::NT + 32, 1)
   }
 }
 
+
 }  // namespace chwb
