@@ -74,3 +74,61 @@ def test_m7_bf16_k1t_variants(cuda, variant):
                         "--rows", "1", "31", "32", "33", "4737"], env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
     assert ("k1t-tma" in p.stdout) == (variant != "0")
+
+
+# ---------------------------------------------------------------------------
+# Boundary cases of the TMA-fed default kernels (K1T m=12, K6 m=16, K4T m=24).
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m,rows", [(12, 300), (16, 150), (24, 2)])
+def test_exact_user_workspace_and_side_stream(cuda, m, rows):
+    """A caller workspace of exactly chw_b200_workspace_bytes() bytes and a
+    non-default stream give the same bits as the library-managed default."""
+    import numpy as np
+    import torch
+
+    import paper_1609_06641_b200 as chw
+
+    g = torch.Generator(device=cuda)
+    g.manual_seed(m * 1000 + rows)
+    x = torch.randn(rows, 1 << m, device=cuda, generator=g)
+    ref = torch.empty_like(x)
+    chw.chw_forward_batched_(x, chw.ScalingMode.Orthonormal, out=ref)
+    need = chw.workspace_bytes(chw.DTYPE_F32, rows, 1 << m)
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device=cuda)
+    side = torch.cuda.Stream()
+    out = torch.empty_like(x)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        chw.chw_forward_batched_(x, chw.ScalingMode.Orthonormal, out=out, stream=side,
+                                 workspace=ws if need else None)
+    side.synchronize()
+    assert torch.equal(out, ref)
+    assert np.isfinite(out.cpu().numpy()).all()
+
+
+@pytest.mark.parametrize("m", [12, 16, 24])
+def test_misaligned_buffers_rejected(cuda, m):
+    """The TMA paths need 16-byte aligned rows; a 4-byte-offset view must be
+    rejected with an argument error, never fault."""
+    import torch
+
+    import paper_1609_06641_b200 as chw
+
+    rows = 2
+    base = torch.zeros(rows * (1 << m) + 4, device=cuda)
+    x = base[1:1 + rows * (1 << m)].view(rows, 1 << m)
+    assert x.data_ptr() % 16 == 4
+    with pytest.raises(ValueError, match="aligned"):
+        chw.chw_forward_batched_(x, chw.ScalingMode.Orthonormal)
+    torch.cuda.synchronize()
+
+
+def test_empty_batch_is_a_no_op(cuda):
+    import torch
+
+    import paper_1609_06641_b200 as chw
+
+    for m in (12, 16, 24):
+        x = torch.zeros(0, 1 << m, device=cuda)
+        chw.chw_forward_batched_(x, chw.ScalingMode.Orthonormal)
+    torch.cuda.synchronize()
