@@ -24,6 +24,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_bf16.h>
 
 #define CHW_HD __host__ __device__ __forceinline__
@@ -471,13 +472,35 @@ __device__ __forceinline__ void bf(long long& a, long long& b) {
 }
 
 
+// Two fp32 butterflies in one packed FADD2 pair (sm_100 add/sub.rn.f32x2):
+// (a0, a1) +/- (b0, b1), each lane rounded exactly like __fadd_rn/__fsub_rn.
+__device__ __forceinline__ void bf2(float& a0, float& a1, float& b0, float& b1) {
+  uint64_t A, B, S, D;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(S) : "l"(A), "l"(B));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(D) : "l"(A), "l"(B));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(S));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(b0), "=f"(b1) : "l"(D));
+}
+
 // Butterflies on the listed tile bits, in list order (order matters only for
-// bit-exact f64; f32/bf16 are order-free up to rounding).
+// bit-exact f64; f32/bf16 are order-free up to rounding).  fp32 butterflies on
+// register bits other than bit 0 are issued in pairs (registers r, r^1) as
+// packed FADD2 instructions: half the FP issue slots, identical results.
 template <class L, class Bits, bool PER_STAGE, class C>
 __device__ __forceinline__ void butterflies(C (&v)[L::E]) {
 #pragma unroll
   for (int i = 0; i < Bits::N; ++i) {
     const int k = L::slot(Bits::at(i));
+    if constexpr (std::is_same<C, float>::value && !PER_STAGE && L::E >= 4) {
+      if (k > 0) {
+#pragma unroll
+        for (int r = 0; r < L::E; r += 2)
+          if (!((r >> k) & 1)) bf2(v[r], v[r | 1], v[r | (1 << k)], v[(r | (1 << k)) | 1]);
+        continue;
+      }
+    }
 #pragma unroll
     for (int r = 0; r < L::E; ++r)
       if (!((r >> k) & 1)) bf<PER_STAGE>(v[r], v[r | (1 << k)]);
