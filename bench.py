@@ -1,21 +1,29 @@
 #!/usr/bin/env python
 """Benchmark: batched CHW (dyadic-order orthonormal WHT) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl ours|reference]
 
-Metric (BASELINE.json): CHW-WHT Gelem/s and HBM GB/s (% of measured peak).
-A "step" is one batched transform of the configuration's whole batch of rows
-(BASELINE.json configs; default cfg2 = configs[1], the config the metric is
-quoted on: 65536 fp32 rows of 2^12, N(0,1)).  Multi-GPU: one process per GPU
-(torchrun), each rank transforms its own 65536-row shard of an N x 65536 global
-batch — rows are independent, so there is no collective on the data path
-(weak scaling); the timed region is bracketed by barrier + synchronize and the
-slowest rank's device time is reported.
+Metric (BASELINE.json): CHW-WHT Gelem/s and HBM GB/s (% of measured peak) at
+1/2/4/8 B200.  A "step" is one batched transform of the configuration's whole
+global batch (BASELINE.json configs).  The default workload is cfg5 (256 fp32
+rows of 2^24, N(0,1)): BASELINE.json names no single config for its metric and
+quotes it "at 1/2/4/8 B200", which covers the sharded configs cfg2 and cfg5;
+cfg5 is the largest single-GPU one.  The other configs are measured in the same
+run under `per_config` (and each is selectable with --config).
+
+Multi-GPU: one process per GPU.  Under torchrun the env (RANK/WORLD_SIZE/...)
+is used; `--gpus N` without it re-launches this script under
+torch.distributed.run.  The FIXED global batch is split into contiguous row
+shards (paper_1609_06641_b200.shard.shard_range: 256/N rows of cfg5, 65536/N
+of cfg2) — strong scaling, no collective on the data path; the timed region is
+bracketed by barrier + synchronize and the slowest rank's device time is used.
 
 ours (default): inputs resident in HBM, kernels launched through the C ABI
   (chw_b200_forward) on the current stream, timed with CUDA events.  `e2e`
   times chw_b200_forward_host (HOST pinned buffers: H2D + kernels + D2H per
-  step) — the reference-facing call.
+  step) — the reference-facing call.  After timing, sampled rows of the timed
+  output are checked against the reference compiled from /root/reference
+  (oracle/_ref, the checker) on the same input bytes (`parity`).
 reference: the reference's own CPU implementation (oracle/_ref/libchw_ref.so:
   the unmodified proj/include headers; else the C restatement) on all host
   cores over a bounded sample of the same workload; rank 0 only.
@@ -26,8 +34,8 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -35,7 +43,7 @@ import time
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-# BASELINE.json configs -> (name, dtype, rows, m, distribution)
+# BASELINE.json configs -> (name, dtype, global rows, m, distribution)
 CONFIGS = {
     "cfg1": ("cfg1: 1024 x 2^10 f64, U[-1,1)", "f64", 1024, 10, "uniform"),
     "cfg2": ("cfg2: 65536 x 2^12 f32, N(0,1)", "f32", 65536, 12, "normal"),
@@ -43,7 +51,11 @@ CONFIGS = {
     "cfg4": ("cfg4: 4096 x 2^16 f32, U[-1,1)", "f32", 4096, 16, "uniform"),
     "cfg5": ("cfg5: 256 x 2^24 f32, N(0,1)", "f32", 256, 24, "normal"),
 }
+DEFAULT_CONFIG = "cfg5"
 ELEM_BYTES = {"f64": 8, "f32": 4, "bf16": 2}
+DTYPE_CODE = {"f64": 0, "f32": 1, "bf16": 2}
+# north_star tolerances (relative L2 per row) for the parity check.
+TOL = {"f64": 1e-12, "f32": 1e-5, "bf16": 1e-2}
 SEED = 1609066410
 
 
@@ -63,6 +75,17 @@ def load_traffic(cfg: str):
             d = json.load(f)
         return d.get(cfg)
     return None
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -136,52 +159,186 @@ def dist_env():
     return world, rank, local
 
 
-def make_input(torch, cfg, rows, dev, rank):
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_distributed(args) -> int:
+    """`--gpus N` outside torchrun: re-run this script as N ranks (one per GPU)."""
+    import subprocess
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def make_input(torch, cfg, first_row, rows, dev):
+    """Rows [first_row, first_row + rows) of the config's synthetic global
+    batch: seeded torch Philox per shard, generated on the device."""
     _, dt, _, m, dist = CONFIGS[cfg]
     g = torch.Generator(device=dev)
-    g.manual_seed(SEED + rank)
+    g.manual_seed(SEED + first_row)
     n = 1 << m
+    if dt == "f64":
+        if dist == "uniform":
+            return (torch.rand(rows, n, generator=g, device=dev, dtype=torch.float64) * 2 - 1).contiguous()
+        return torch.randn(rows, n, generator=g, device=dev, dtype=torch.float64).contiguous()
     if dist == "normal":
         x = torch.randn(rows, n, generator=g, device=dev, dtype=torch.float32)
     else:
         x = torch.rand(rows, n, generator=g, device=dev, dtype=torch.float32) * 2 - 1
-    tdt = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dt]
-    if dt == "f64":
-        x = (torch.rand(rows, n, generator=g, device=dev, dtype=torch.float64) * 2 - 1) if dist == "uniform" \
-            else torch.randn(rows, n, generator=g, device=dev, dtype=torch.float64)
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[dt]
     return x.to(tdt).contiguous()
 
 
-def cpu_reference_rate(cfg: str, rows: int, reps: int = 1, threads: int = 0):
-    """Reference CPU implementation (oracle/_ref if built, else the C port) on
-    all host cores; returns (Gelem/s best-of-reps, kind, cores, sample text)."""
+# ---------------------------------------------------------------------------
+# Checker (oracle/ is test infrastructure: used here only to CHECK the timed
+# output and to time the CPU baseline, never as the thing measured).
+# ---------------------------------------------------------------------------
+def sample_rows(rows: int, want: int = 8):
+    """Row indices spread over the batch: first/last rows, the first and last
+    chunk of the m = 24 schedule, CTA-boundary rows (multiples of 148)."""
+    cand = [0, 1, rows // 2, rows - 2, rows - 1, 15, 16, 147, 148, 149, rows // 3, (2 * rows) // 3,
+            rows - 17, rows - 16]
+    out = []
+    for r in cand:
+        if 0 <= r < rows and r not in out:
+            out.append(r)
+        if len(out) >= want:
+            break
+    return sorted(out)
+
+
+def check_parity(torch, chw, cfg, x, out, rows_checked=8):
+    """Compare sampled rows of the timed output with the reference (oracle/_ref
+    when built, else the C port) on the same input bytes, plus an exact
+    integer order probe through the same kernel path."""
+    import numpy as np
+
+    import oracle
+
+    name, dt, _, m, _ = CONFIGS[cfg]
+    n = 1 << m
+    rows = x.shape[0]
+    if rows == 0:
+        return {"rows_checked": 0, "max_rel_l2": 0.0, "tolerance": TOL[dt], "order_probe_ok": True, "ok": True}
+    backend = "reference" if oracle.have_reference() else "port"
+    idx = sample_rows(rows, rows_checked)
+    it = torch.tensor(idx, device=x.device)
+    xs = x.index_select(0, it).to(torch.float64).cpu().numpy()  # exact upcast of the input bytes
+    ys = out.index_select(0, it).to(torch.float64).cpu().numpy()
+    ref = oracle.chw_batch(xs, oracle.ORTHONORMAL, backend=backend, threads=len(idx))
+    rel = np.linalg.norm(ys - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-300)
+    res = {"rows_checked": len(idx), "rows": idx, "checker": backend, "max_rel_l2": float(rel.max()),
+           "tolerance": TOL[dt]}
+    if dt == "f64":
+        res["bit_exact"] = bool(np.array_equal(ys.view(np.uint64), ref.view(np.uint64)))
+    # Exact order probe: integer inputs, Unnormalized, every partial sum exact
+    # (|x| <= 2^(24-m) for f32, {-1,0,1} for bf16 at m <= 7, 2^(53-m) for f64):
+    # the output must equal the int64 reference bit for bit.
+    bound = {"f32": 1 << max(0, 24 - m), "bf16": 1 if m <= 7 else 0, "f64": 1 << min(20, 53 - m)}[dt]
+    if bound:
+        pr = min(rows, 3 if m >= 20 else 64)
+        rng = np.random.default_rng(SEED + 7)
+        xi = rng.integers(-bound, bound + 1, size=(pr, n), dtype=np.int64)
+        tdt = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dt]
+        d = torch.from_numpy(xi).to(x.device).to(tdt)
+        chw.chw_forward_batched_(d, chw.ScalingMode.Unnormalized)
+        got = d.to(torch.float64).cpu().numpy()
+        want = oracle.chw_batch(xi, oracle.UNNORMALIZED, backend=backend, threads=pr)
+        res["order_probe_rows"] = pr
+        res["order_probe_ok"] = bool(np.array_equal(got, want.astype(np.float64)))
+        del d
+    else:
+        res["order_probe_ok"] = None
+    res["ok"] = bool(res["max_rel_l2"] <= TOL[dt] and res["order_probe_ok"] is not False
+                     and res.get("bit_exact", True))
+    return res
+
+
+_SAMPLES = {}
+
+
+def _ref_rate(cfg: str, rows: int, threads: int, reps: int):
+    """Reference chw_forward_inplace<double> Orthonormal per row over `rows`
+    sample rows on `threads` host threads; returns (best Gelem/s, best s, kind)."""
     import numpy as np
 
     import oracle
 
     _, dt, _, m, dist = CONFIGS[cfg]
     n = 1 << m
-    rng = np.random.default_rng(SEED)
-    x = rng.standard_normal((rows, n)) if dist == "normal" else rng.uniform(-1, 1, (rows, n))
-    if dt == "f32":
-        x = x.astype(np.float32).astype(np.float64)  # exact upcast of the fp32 bytes
-    elif dt == "bf16":
-        import torch
+    key = (cfg, rows)
+    x = _SAMPLES.get(key)
+    if x is None:
+        rng = np.random.default_rng(SEED)
+        x = rng.standard_normal((rows, n)) if dist == "normal" else rng.uniform(-1, 1, (rows, n))
+        if dt == "f32":
+            x = x.astype(np.float32).astype(np.float64)  # exact upcast of the fp32 bytes
+        elif dt == "bf16":
+            import torch
 
-        x = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
-    x = np.ascontiguousarray(x)
+            x = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+        x = np.ascontiguousarray(x)
+        _SAMPLES.clear()
+        _SAMPLES[key] = x
     kind = "reference" if oracle.have_reference() else "port"
-    cores = threads if threads > 0 else (os.cpu_count() or 1)
     best = math.inf
     for _ in range(reps):
         buf = x.copy()
         t0 = time.perf_counter()
-        oracle.chw_batch_inplace(buf, oracle.ORTHONORMAL, backend=kind, threads=cores)
+        oracle.chw_batch_inplace(buf, oracle.ORTHONORMAL, backend=kind, threads=threads)
         best = min(best, time.perf_counter() - t0)
-    gel = rows * n / best / 1e9
-    sample = (f"{rows} rows x 2^{m} of {cfg}, reference chw_forward_inplace<double> Orthonormal per row, "
-              f"rows split over {cores} threads, best of {reps}; input upcast to f64 outside the timer")
-    return gel, kind, cores, sample, best
+    return rows * n / best / 1e9, best, kind
+
+
+def _sample_rows_for(cfg: str, cores: int, target_elems: int) -> int:
+    _, _, rows_full, m, _ = CONFIGS[cfg]
+    return max(1, min(rows_full, max(cores, target_elems >> m)))
+
+
+def cpu_baseline(cfg: str):
+    """SURVEY §8(d) CPU baseline: the reference on all host cores (best of 3),
+    on 1 core, and (cfg5) the paper's own executor parallel_execute_inplace on
+    one row with workers = cores.  Bounded to ~10-30 s of CPU work."""
+    import numpy as np
+
+    import oracle
+
+    _, dt, _, m, _ = CONFIGS[cfg]
+    n = 1 << m
+    cores = os.cpu_count() or 1
+    rows_all = _sample_rows_for(cfg, cores, 1 << 26)
+    gel_all, _, kind = _ref_rate(cfg, rows_all, cores, 3)
+    rows_one = max(1, min(CONFIGS[cfg][2], (1 << 24) >> m))
+    gel_one, _, _ = _ref_rate(cfg, rows_one, 1, 1)
+    res = {"value": round(gel_all, 4), "unit": "Gelem/s", "cores": cores, "kind": kind,
+           "cpu_model": cpu_model(), "best_of": 3,
+           "sample": (f"{rows_all} rows x 2^{m} of {cfg}, reference chw_forward_inplace<double> Orthonormal "
+                      f"per row, rows split over {cores} threads (one scratch each), best of 3; input "
+                      f"({dt}) upcast to f64 outside the timer (the reference has only int64/double)"),
+           "one_core": {"value": round(gel_one, 4), "unit": "Gelem/s", "sample": f"{rows_one} rows x 2^{m}, 1 thread"}}
+    if cfg == "cfg5" and kind == "reference":
+        ref = oracle.reference()
+        rng = np.random.default_rng(SEED)
+        row = np.ascontiguousarray(rng.standard_normal(n).astype(np.float32).astype(np.float64))
+        adds = __import__("ctypes").c_uint64(0)
+        mults = __import__("ctypes").c_uint64(0)
+        t0 = time.perf_counter()
+        rc = ref.fn("parallel_execute_f64")(row.ctypes.data_as(oracle._dp), n, cores, oracle.ORTHONORMAL,
+                                           __import__("ctypes").byref(adds), __import__("ctypes").byref(mults))
+        dt_s = time.perf_counter() - t0
+        if rc == 0:
+            res["parallel_execute"] = {"value": round(n / dt_s / 1e9, 5), "unit": "Gelem/s", "workers": cores,
+                                       "seconds": round(dt_s, 3),
+                                       "sample": "one 2^24 row, reference parallel_execute_inplace<double> "
+                                                 "(the paper's node-per-scale executor, parallel.cpp:84-103)"}
+    return res
 
 
 def run_reference(args):
@@ -191,28 +348,91 @@ def run_reference(args):
     cfg = args.config
     name, dt, rows_full, m, _ = CONFIGS[cfg]
     n = 1 << m
-    # bounded sample per step: ~128M elements (or the whole batch if smaller)
-    rows = max(1, min(rows_full, (1 << 27) >> m))
+    cores = os.cpu_count() or 1
+    # bounded sample per step: one row per core (or ~64M elements for short rows)
+    rows = _sample_rows_for(cfg, cores, 1 << 26)
+    wrows = max(1, min(rows, cores))
     for _ in range(args.warmup):
-        cpu_reference_rate(cfg, max(1, rows // 8))
+        _ref_rate(cfg, wrows if m >= 20 else rows, cores, 1)
     times = []
+    kind = "port"
     for _ in range(args.steps):
-        gel, kind, cores, sample, t = cpu_reference_rate(cfg, rows)
+        _, t, kind = _ref_rate(cfg, rows, cores, 1)
         times.append(t)
     tot = sum(times)
     value = args.steps * rows * n / tot / 1e9
+    sample = (f"{rows} rows x 2^{m} of {cfg} per step, reference chw_forward_inplace<double> Orthonormal per "
+              f"row, rows split over {cores} threads; input upcast to f64 outside the timer")
     line = {
         "impl": "reference", "metric": "CHW-WHT Gelem/s", "value": round(value, 4), "unit": "Gelem/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": f"synthetic seed {SEED}",
-        "config": {"workload": name, "global_batch": rows_full * world, "n": n, "rows_per_step": rows},
+        "config": {"workload": name, "global_batch": rows_full, "n": n, "rows_per_step": rows},
         "cpu_baseline": {"value": round(value, 4), "unit": "Gelem/s", "cores": cores, "kind": kind,
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def time_config(torch, chw, cfg, first, rows, dev, steps, warmup, soak_s=0.0, order="dyadic", sampler=None,
+                barrier=None):
+    """Time `steps` transforms of this rank's rows of `cfg` (inputs resident in
+    HBM); returns a dict with per-step device times and the buffers."""
+    name, dt, _, m, _ = CONFIGS[cfg]
+    n = 1 << m
+    es = ELEM_BYTES[dt]
+    x = make_input(torch, cfg, first, rows, dev)
+    out = torch.empty_like(x)
+    ordc = {"dyadic": chw.ORDER_DYADIC, "natural": chw.ORDER_NATURAL, "sequency": chw.ORDER_SEQUENCY}[order]
+    ws_bytes = chw.workspace_bytes_ordered(DTYPE_CODE[dt], rows, n, ordc) if rows else 0
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    barrier = barrier or torch.cuda.synchronize
+
+    def step():
+        if rows:
+            chw.chw_forward_batched_(x, chw.ScalingMode.Orthonormal, out=out, stream=stream,
+                                     workspace=ws if ws_bytes else None, order=ordc)
+
+    # L2 policy: footprints much larger than L2 need no flush; smaller ones get
+    # a flush write (and a clean read that writes its dirty lines back) before
+    # every timed step.
+    footprint = 2 * rows * n * es
+    flush = clean = None
+    if footprint < 4 * 126 * 2**20:
+        flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
+        clean = torch.ones(64 * 2**20, dtype=torch.float32, device=dev)
+    for _ in range(max(3, warmup)):
+        step()
+    barrier()
+    t_end = time.time() + soak_s  # untimed load so NVML sees the clocks under load
+    while time.time() < t_end:
+        for _ in range(8):
+            step()
+        torch.cuda.synchronize()
+    barrier()
+    launches0 = chw.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    t0.record(stream)
+    for i in range(steps):
+        if flush is not None:
+            flush.zero_()
+            clean.sum()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    t1.record(stream)
+    barrier()
+    launches = chw.launch_count() - launches0
+    kern_ms = [a.elapsed_time(b) for a, b in evs]
+    return {"x": x, "out": out, "kern_ms": kern_ms, "region_ms": t0.elapsed_time(t1), "launches": launches,
+            "flush": flush is not None, "alg_bytes": 2 * rows * n * es}
 
 
 def run_ours(args):
@@ -220,90 +440,66 @@ def run_ours(args):
     import torch.distributed as tdist
 
     import paper_1609_06641_b200 as chw
+    from paper_1609_06641_b200.shard import shard_range
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    # More ranks than GPUs (a functional run of the multi-rank path on a
+    # smaller box): ranks share devices and use gloo for the host-side
+    # barriers; the timing is then not a scaling number (config.shared_gpu).
+    shared = world > ndev
+    local_dev = local % max(1, ndev)
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=dev)
+        if shared:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=dev)
+    coll_dev = torch.device("cpu") if shared else dev
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
             tdist.barrier()
         torch.cuda.synchronize()
 
+    def max_ranks(v: float) -> float:
+        t = torch.tensor([v], device=coll_dev, dtype=torch.float64)
+        if world > 1:
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
     cfg = args.config
-    name, dt, rows, m, dist_name = CONFIGS[cfg]
+    name, dt, rows_global, m, dist_name = CONFIGS[cfg]
     n = 1 << m
     es = ELEM_BYTES[dt]
-    x = make_input(torch, cfg, rows, dev, rank)
-    out = torch.empty_like(x)
-    ws_bytes = chw.workspace_bytes({"f64": 0, "f32": 1, "bf16": 2}[dt], rows, n)
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
-
-    order = {"dyadic": chw.ORDER_DYADIC, "natural": chw.ORDER_NATURAL}[args.order]
-
-    def step():
-        chw.chw_forward_batched_(x, chw.ScalingMode.Orthonormal, out=out, stream=stream,
-                                 workspace=ws if ws_bytes else None, order=order)
-
-    # L2 policy: inputs larger than L2 need no flush; smaller ones get a flush write between steps.
-    footprint = 2 * rows * n * es
-    flush = None
-    if footprint < 4 * 126 * 2**20:
-        flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
-        # A write flush leaves L2 full of dirty lines whose write-back would land
-        # inside the next timed step; reading a second clean buffer afterwards
-        # evicts them before the step starts (the step still starts cold).
-        clean = torch.ones(64 * 2**20, dtype=torch.float32, device=dev)
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    barrier()
-
-    # clock soak: keep the GPU busy ~1 s before the timed region so NVML sees load
-    sampler = ClockSampler(local)
-    with sampler:
-        t_end = time.time() + args.soak
-        while time.time() < t_end:
-            for _ in range(8):
-                step()
-            torch.cuda.synchronize()
-        barrier()
-        launches0 = chw.launch_count()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-        barrier()
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_stop = torch.cuda.Event(enable_timing=True)
-        t_start.record(stream)
-        for i in range(args.steps):
-            if flush is not None:
-                flush.zero_()
-                clean.sum()
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
-        t_stop.record(stream)
-        barrier()
-        launches = chw.launch_count() - launches0
-    kern_ms = [a.elapsed_time(b) for a, b in evs]
-    total_kern_ms = sum(kern_ms)
-    wall_region_ms = t_start.elapsed_time(t_stop)
-    t = torch.tensor([total_kern_ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    max_ms = float(t.item())
-    ms_per_step = max_ms / args.steps
-    elems_all = rows * n * world
-    value = elems_all / (ms_per_step * 1e-3) / 1e9
-
-    # roofline of the dominant kernel family (all launches of one step = the transform)
+    first, rows = shard_range(rows_global, world, rank)
     peak, peak_src = load_peaks()
-    alg_bytes = 2 * rows * n * es
-    achieved = alg_bytes / (statistics.mean(kern_ms) * 1e-3) / 1e9
+
+    sampler = ClockSampler(local_dev)
+    with sampler:
+        r = time_config(torch, chw, cfg, first, rows, dev, args.steps, args.warmup, soak_s=args.soak,
+                        order=args.order, barrier=barrier)
+    clocks = sampler.summary()
+    kern_ms = r["kern_ms"]
+    max_ms = max_ranks(sum(kern_ms))
+    ms_per_step = max_ms / args.steps
+    value = rows_global * n / (ms_per_step * 1e-3) / 1e9
+    # roofline of the dominant kernel family (all launches of one step = the transform)
+    achieved = r["alg_bytes"] / (statistics.mean(kern_ms) * 1e-3) / 1e9 if rows else 0.0
     traffic = load_traffic(cfg)
+    x, out = r["x"], r["out"]
+    launches, region_ms, flushed = r["launches"], r["region_ms"], r["flush"]
+
+    # parity of the timed output (checker), every rank on its own rows
+    parity = None
+    if not args.no_parity:
+        parity = check_parity(torch, chw, cfg, x, out)
+        bad = max_ranks(0.0 if parity["ok"] else 1.0)
+        worst = max_ranks(parity["max_rel_l2"])
+        parity["ok_all_ranks"] = bad == 0.0
+        parity["max_rel_l2_all_ranks"] = worst
 
     # copy peak in the same run (K0): one read + one write of a 1 GiB buffer
     a = torch.empty(2**30, dtype=torch.uint8, device=dev)
@@ -323,58 +519,81 @@ def run_ours(args):
     del a, b
 
     # e2e through the host-buffer C-ABI call (pinned host in/out, H2D + kernels + D2H)
-    hx = x.cpu().pin_memory()
-    hy = torch.empty_like(hx).pin_memory()
-    e2e_steps = max(2, min(args.steps, args.e2e_steps))
-    chw.chw_forward_host_(hx, chw.ScalingMode.Orthonormal, out=hy)  # warm-up (allocates staging)
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        chw.chw_forward_host_(hx, chw.ScalingMode.Orthonormal, out=hy)
-    e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-    if world > 1:
-        tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
-    e2e_value = elems_all * e2e_steps / float(te.item()) / 1e9
-    # e2e result must equal the device result
-    e2e_ok = bool(torch.equal(hy.to(dev), out))
+    e2e = None
+    if rows:
+        hx = x.cpu().pin_memory()
+        hy = torch.empty_like(hx).pin_memory()
+        e2e_steps = max(2, min(args.steps, args.e2e_steps))
+        chw.chw_forward_host_(hx, chw.ScalingMode.Orthonormal, out=hy)  # warm-up (allocates staging)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            chw.chw_forward_host_(hx, chw.ScalingMode.Orthonormal, out=hy)
+        e2e_s = max_ranks(time.perf_counter() - t0)
+        e2e_ok = bool(torch.equal(hy.to(dev), out))
+        e2e = {"value": round(rows_global * n * e2e_steps / e2e_s / 1e9, 3), "unit": "Gelem/s",
+               "h2d_bytes_per_step": rows * n * es, "d2h_bytes_per_step": rows * n * es,
+               "matches_device_result": e2e_ok, "steps": e2e_steps}
+        del hx, hy
+    del x, out, r
+    torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu_rows = rows if cfg != "cfg5" else 2
-        gel, kind, cores, sample, _ = cpu_reference_rate(cfg, min(rows, cpu_rows), reps=1)
-        cpu = {"value": round(gel, 4), "unit": "Gelem/s", "cores": cores, "kind": kind, "sample": sample}
+        cpu = cpu_baseline(cfg)
+
+    # the other BASELINE configs, same protocol (N = 1 only)
+    per_config = None
+    if world == 1 and not args.no_per_config:
+        per_config = {}
+        for c in sorted(CONFIGS):
+            if c == cfg:
+                continue
+            cn, cdt, crows, cm, _ = CONFIGS[c]
+            rc = time_config(torch, chw, c, 0, crows, dev, max(10, args.steps), 3)
+            ms = statistics.mean(rc["kern_ms"])
+            pc = check_parity(torch, chw, c, rc["x"], rc["out"]) if not args.no_parity else None
+            per_config[c] = {
+                "workload": cn, "value": round(crows * (1 << cm) / (ms * 1e-3) / 1e9, 3), "unit": "Gelem/s",
+                "ms_per_step": round(ms, 4), "frac": round(rc["alg_bytes"] / (ms * 1e-3) / 1e9 / peak, 4),
+                "plan": chw.plan_name(DTYPE_CODE[cdt], 1 << cm), "l2_flush": rc["flush"],
+                "traffic": load_traffic(c),
+                "parity": None if pc is None else {k: pc[k] for k in ("rows_checked", "max_rel_l2", "tolerance",
+                                                                       "order_probe_ok", "ok")},
+            }
+            del rc
+            torch.cuda.empty_cache()
 
     if rank == 0:
-        clocks = sampler.summary()
         line = {
             "metric": "CHW-WHT Gelem/s", "value": round(value, 3), "unit": "Gelem/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dt,
-            "data": f"synthetic {dist_name} (torch Philox, seed {SEED}+rank), generated on device",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dt,
+            "data": f"synthetic {dist_name} (torch Philox, seed {SEED}+first row of the shard), generated on device",
             "config": {
-                "workload": name, "global_batch": rows * world, "per_rank_batch": rows, "n": n,
-                "parallelism": f"batch-sharded x{world}, no collective on the data path",
-                "l2": "inputs+outputs larger than L2 (no flush)" if flush is None
+                "workload": name, "global_batch": rows_global, "per_rank_batch": rows, "n": n,
+                "parallelism": f"batch-sharded x{world} (shard_range: contiguous rows), no collective on the data path",
+                "l2": "inputs+outputs larger than L2 (no flush)" if not flushed
                 else "L2 flushed before every timed step (256 MiB write, then a 256 MiB read that writes the "
                 "flush's dirty lines back outside the timed region)",
-                "plan": chw.plan_name({"f64": 0, "f32": 1, "bf16": 2}[dt], n) if args.order == "dyadic"
-                else "natural-order k1 generic",
+                "plan": chw.plan_name(DTYPE_CODE[dt], n) if args.order == "dyadic" else f"{args.order}-order",
                 "order": args.order,
+                "shared_gpu": shared,
             },
             "hbm_gbs": round(achieved, 1), "pct_of_peak": round(100 * achieved / peak, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes,
+                         "peak_source": peak_src, "alg_bytes_per_launch": rows * n * es * 2,
                          "copy_peak_same_run_gbs": round(copy_peak, 1)},
             "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_value, 3), "unit": "Gelem/s",
-                    "h2d_bytes_per_step": rows * n * es, "d2h_bytes_per_step": rows * n * es,
-                    "matches_device_result": e2e_ok, "steps": e2e_steps},
+            "e2e": e2e,
+            "parity": parity,
             "gpu_launches": launches,
             "clocks": clocks,
-            "timed_region_ms": round(wall_region_ms, 3),
+            "timed_region_ms": round(region_ms, 3),
         }
+        if per_config is not None:
+            line["per_config"] = per_config
         print(json.dumps(line), flush=True)
     if world > 1:
         tdist.barrier()
@@ -388,15 +607,19 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of untimed load before timing")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--order", default="dyadic", choices=["dyadic", "natural"],
-                    help="output order (the BASELINE metric is dyadic; natural is for experiments)")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--order", default="dyadic", choices=["dyadic", "natural", "sequency"],
+                    help="output order (the BASELINE metric is dyadic; others are for experiments)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

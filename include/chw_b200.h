@@ -32,8 +32,11 @@
  * exception types.
  *
  * Thread safety: calls on different streams / disjoint buffers may run
- * concurrently; there is no global mutable state visible to the
- * caller besides the per-device workspace cache, which is internally locked.
+ * concurrently.  A call made with workspace == NULL gets its own
+ * stream-ordered scratch (cudaMallocFromPoolAsync on the caller's stream from a
+ * private per-device pool, freed on that stream after its launches), so two
+ * such calls never share scratch.  The host-buffer calls are synchronous and
+ * serialised per device by an internal lock.
  */
 #ifndef CHW_B200_H
 #define CHW_B200_H
@@ -140,6 +143,13 @@ chw_status chw_b200_haar_forward_host(const void* in_host, void* out_host, chw_d
 /* Host-buffer call with an explicit output order. */
 chw_status chw_b200_forward_host_ordered(const void* in_host, void* out_host, chw_dtype dtype,
                                          int64_t batch, uint64_t n, chw_mode mode, chw_order order);
+
+/* Device path of chw::normalize_inplace (proj/include/chw/transforms.hpp:202-210)
+ * on `batch` rows of n = 2^m elements: x *= 1/sqrt(2^m), the reference's own
+ * constant and one multiply per element (f64 bit-exact; F32 also accepted).
+ * n != 2^m -> CHW_ERR_LENGTH with the reference's message.  Asynchronous on
+ * `stream`; the buffer must be 16-byte aligned. */
+chw_status chw_b200_normalize(void* x, chw_dtype dtype, int64_t batch, uint64_t n, int m, void* stream);
 
 /* parallel_execute_inplace(x, workers, mode) on a DEVICE buffer of one signal.
  * Validation as parallel.cpp:84-91; the pool is replaced by the GPU. */

@@ -291,8 +291,14 @@ inline void normalize_inplace(std::span<double> x, int m, OpTally* tally = nullp
     throw std::invalid_argument("normalize: signal length " + std::to_string(x.size()) +
                                 " does not match level " + std::to_string(m));
   }
-  const double c = 1.0 / std::sqrt(std::ldexp(1.0, m));
-  for (double& v : x) v *= c;
+  if (!x.empty() && chw_b200_is_device_pointer(x.data())) {
+    // Device span: one multiply per element on the GPU (bit-identical), synchronous.
+    detail::raise(chw_b200_normalize(x.data(), CHW_F64, 1, x.size(), m, nullptr));
+    detail::raise(chw_b200_stream_synchronize(nullptr));
+  } else {
+    const double c = 1.0 / std::sqrt(std::ldexp(1.0, m));
+    for (double& v : x) v *= c;
+  }
   if (tally) tally->multiplications += x.size();
 }
 

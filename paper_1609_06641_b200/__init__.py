@@ -72,6 +72,7 @@ EXPORTED_SYMBOLS = (
     "chw_b200_haar_inverse_host",
     "chw_b200_haar_walsh_forward_host",
     "chw_b200_stream_synchronize",
+    "chw_b200_normalize",
 )
 
 
@@ -178,6 +179,8 @@ def _load() -> ctypes.CDLL:
     lib.chw_b200_is_device_pointer.restype = c.c_int
     lib.chw_b200_stream_synchronize.argtypes = [c.c_void_p]
     lib.chw_b200_stream_synchronize.restype = c.c_int
+    lib.chw_b200_normalize.argtypes = [c.c_void_p, c.c_int, c.c_int64, c.c_uint64, c.c_int, c.c_void_p]
+    lib.chw_b200_normalize.restype = c.c_int
     return lib
 
 
@@ -360,6 +363,10 @@ def chw_forward_host_(x, mode: ScalingMode = ScalingMode.Orthonormal, tally: Opt
         numel = x.numel()
         if not x.is_contiguous():
             raise ValueError("chw_forward: expected a contiguous tensor")
+        if out is not None and (not isinstance(out, torch.Tensor) or out.is_cuda or out.shape != x.shape
+                                or out.dtype != x.dtype or not out.is_contiguous()):
+            raise ValueError("chw_forward: `out` must be a host tensor matching the input's shape, "
+                             "dtype and layout")
         dst_ptr = out.data_ptr() if out is not None else arr_ptr
     else:
         if not isinstance(x, np.ndarray):
@@ -374,6 +381,11 @@ def chw_forward_host_(x, mode: ScalingMode = ScalingMode.Orthonormal, tally: Opt
         arr_ptr = x.ctypes.data
         n = int(x.shape[-1]) if x.ndim > 0 else 1
         numel = x.size
+        if out is not None and (not isinstance(out, np.ndarray) or out.shape != x.shape
+                                or out.dtype != x.dtype or not out.flags["C_CONTIGUOUS"]
+                                or not out.flags["WRITEABLE"]):
+            raise ValueError("chw_forward: `out` must be a writable array matching the input's shape, "
+                             "dtype and layout")
         dst_ptr = out.ctypes.data if out is not None else arr_ptr
     batch = numel // n if n > 0 else 0
     if n == 0:
@@ -534,9 +546,24 @@ def normalize_inplace(x, m: int, tally: Optional[OpTally] = None):
         raise ValueError(f"normalize: signal length {n} does not match level {m}")
     import math
 
-    x *= 1.0 / math.sqrt(math.ldexp(1.0, m))
+    torch = _torch()
+    rows = 1
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        # Device path: one multiply per element in the library's kernel
+        # (chw_b200_normalize; bit-identical to the reference loop for f64).
+        if not x.is_contiguous():
+            raise ValueError("normalize: expected a contiguous tensor")
+        rows = x.numel() // n if n else 0
+        with torch.cuda.device(x.device):
+            _check(lib.chw_b200_normalize(x.data_ptr(), dtype_code(x), rows, n, m,
+                                          _stream_ptr(None)))
+        torch.cuda.current_stream().synchronize()
+    else:
+        if hasattr(x, "shape") and len(x.shape) > 1:
+            rows = int(__import__("numpy").prod(x.shape[:-1]))
+        x *= 1.0 / math.sqrt(math.ldexp(1.0, m))
     if tally is not None:
-        tally.multiplications += int(n)
+        tally.multiplications += int(n) * rows
     return x
 
 
@@ -580,6 +607,10 @@ def workspace_bytes(dtype: int, batch: int, n: int) -> int:
     return int(lib.chw_b200_workspace_bytes(dtype, batch, n))
 
 
+def workspace_bytes_ordered(dtype: int, batch: int, n: int, order: int) -> int:
+    return int(lib.chw_b200_workspace_bytes_ordered(dtype, batch, n, order))
+
+
 def plan_name(dtype: int, n: int) -> str:
     return lib.chw_b200_plan_name(dtype, n).decode()
 
@@ -595,6 +626,6 @@ __all__ = [
     "haar_inverse", "haar_inverse_inplace", "haar_walsh_forward", "haar_walsh_forward_inplace",
     "StructureError", "fwht_natural", "fwht_natural_inplace", "fwht_dyadic", "fwht_dyadic_inplace", "chw_forward_sequency",
     "parallel_execute", "parallel_execute_inplace", "normalize_inplace", "normalized",
-    "stage_blocks", "bit_reverse", "natural_to_dyadic", "workspace_bytes", "plan_name",
+    "stage_blocks", "bit_reverse", "natural_to_dyadic", "workspace_bytes", "workspace_bytes_ordered", "plan_name",
     "launch_count", "lib", "LIB_PATH", "EXPORTED_SYMBOLS",
 ]

@@ -108,8 +108,8 @@ double ortho_scale(int m) {
 // Per-device state: SM count, lazily-grown workspace, streams for the host path.
 // ---------------------------------------------------------------------------
 struct DeviceState {
-  std::mutex mu;
-  void* ws = nullptr;
+  std::mutex mu;  // serialises host-buffer calls (they own everything below)
+  void* ws = nullptr;  // host path only: per-chunk workspaces of its two streams
   size_t ws_bytes = 0;
   int sms = 0;
   // host path
@@ -122,25 +122,88 @@ struct DeviceState {
 };
 DeviceState g_dev[64];
 
-chw_status ensure_workspace(int dev, size_t bytes, void** out) {
-  DeviceState& s = g_dev[dev];
-  std::lock_guard<std::mutex> lk(s.mu);
-  if (s.ws_bytes < bytes) {
-    if (s.ws) {
-      cudaDeviceSynchronize();  // the old workspace may still be in use by queued work
-      cudaFree(s.ws);
-      s.ws = nullptr;
-      s.ws_bytes = 0;
-    }
-    cudaError_t e = cudaMalloc(&s.ws, bytes);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(CHW_ERR_RESOURCE, "chw_forward: cannot allocate " + std::to_string(bytes) +
-                                        " bytes of workspace: " + cudaGetErrorString(e));
-    }
-    s.ws_bytes = bytes;
+// Library-managed scratch for calls made with workspace == NULL: stream-ordered
+// allocations from a private per-device memory pool (cudaMallocFromPoolAsync
+// on the caller's stream, cudaFreeAsync on the same stream after the last
+// launch that uses it).  Concurrent calls on different streams therefore get
+// disjoint buffers, and a buffer is reused only after the work that used it
+// has completed in stream order — the reference's "concurrent calls on
+// disjoint buffers are safe" contract without a shared buffer.
+// The pool keeps its memory (release threshold = max), so steady-state calls
+// do not reach the driver's allocator.
+cudaMemPool_t g_pool[64] = {};
+std::mutex g_pool_mu;
+
+chw_status ws_pool(int dev, cudaMemPool_t* out) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    CHW_CUDA(cudaMemPoolCreate(&p, &props));
+    uint64_t thr = ~0ull;
+    CHW_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_pool[dev] = p;
   }
-  *out = s.ws;
+  *out = g_pool[dev];
+  return CHW_OK;
+}
+
+// RAII lease: `p` is the caller's workspace or a stream-ordered allocation
+// that is released on `st` when the lease goes out of scope (after the
+// launches that use it have been enqueued).
+struct WsLease {
+  void* p = nullptr;
+  bool owned = false;
+  cudaStream_t st = nullptr;
+  WsLease() = default;
+  WsLease(const WsLease&) = delete;
+  WsLease& operator=(const WsLease&) = delete;
+  ~WsLease() {
+    if (owned && p) cudaFreeAsync(p, st);
+  }
+};
+
+chw_status lease_workspace(const char* what, size_t need, void* caller_ws, size_t caller_bytes, cudaStream_t st,
+                           WsLease* lease) {
+  lease->st = st;
+  if (need == 0) {
+    lease->p = caller_ws;
+    return CHW_OK;
+  }
+  if (caller_ws) {
+    if (caller_bytes < need)
+      return fail(CHW_ERR_WORKSPACE, std::string(what) + ": workspace of " + std::to_string(caller_bytes) +
+                                         " bytes is smaller than the " + std::to_string(need) + " required");
+    lease->p = caller_ws;
+    return CHW_OK;
+  }
+  int dev = 0;
+  if (chw_status s = current_device(&dev)) return s;
+  cudaMemPool_t pool = nullptr;
+  if (chw_status s = ws_pool(dev, &pool)) return s;
+  void* p = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&p, need, pool, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CHW_ERR_RESOURCE, std::string(what) + ": cannot allocate " + std::to_string(need) +
+                                      " bytes of workspace: " + cudaGetErrorString(e));
+  }
+  lease->p = p;
+  lease->owned = true;
+  return CHW_OK;
+}
+
+// The kernels move 16-byte vectors and TMA tiles: every device buffer must be
+// 16-byte aligned (cudaMalloc and torch allocations are).  Checked once here,
+// before any launch, so a misaligned view returns CHW_ERR_ARGUMENT instead of
+// raising a sticky cudaErrorMisalignedAddress.
+chw_status check_aligned(const char* what, const void* a, const void* b, const void* c) {
+  if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 15u)
+    return fail(CHW_ERR_ARGUMENT, std::string(what) + ": buffers and workspace must be 16-byte aligned");
   return CHW_OK;
 }
 
@@ -161,9 +224,13 @@ size_t workspace_for(chw_dtype dtype, int64_t batch, int m) {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+int k1max_of(chw_dtype dtype);
+
 size_t ordered_workspace(chw_dtype dtype, int64_t batch, int m, chw_order order) {
   const size_t inner = workspace_for(dtype, batch, m);
   if (order == CHW_ORDER_DYADIC || batch <= 0) return inner;
+  // Natural order on single-pass sizes is the kernel's store map: no gather buffer.
+  if (order == CHW_ORDER_NATURAL && m <= k1max_of(dtype)) return inner;
   return align256(inner) + (size_t)batch * ((size_t)1 << m) * elem_size(dtype);
 }
 
@@ -212,18 +279,10 @@ chw_status forward_impl(const void* in, void* out, chw_dtype dtype, int64_t batc
   if (!in || !out) return fail(CHW_ERR_ARGUMENT, "chw_forward: null buffer");
   const int m = level_of(n);
   const size_t need = ordered_workspace(dtype, batch, m, order);
-  void* ws = workspace;
-  if (need > 0) {
-    if (ws == nullptr) {
-      int dev = 0;
-      if (chw_status s = current_device(&dev)) return s;
-      if (chw_status s = ensure_workspace(dev, need, &ws)) return s;
-    } else if (workspace_bytes < need) {
-      return fail(CHW_ERR_WORKSPACE, "chw_forward: workspace of " + std::to_string(workspace_bytes) +
-                                         " bytes is smaller than the " + std::to_string(need) +
-                                         " required");
-    }
-  }
+  if (chw_status s = check_aligned("chw_forward", in, out, need ? workspace : nullptr)) return s;
+  WsLease lease;
+  if (chw_status s = lease_workspace("chw_forward", need, workspace, workspace_bytes, st, &lease)) return s;
+  void* ws = lease.p;
   if (order == CHW_ORDER_DYADIC) return dyadic_impl(in, out, dtype, batch, m, mode, ws, st);
   // Natural order for single-pass sizes: the order is the kernel's store map.
   if (order == CHW_ORDER_NATURAL && m <= k1max_of(dtype)) return natural_k1_impl(in, out, dtype, batch, m, mode, st);
@@ -321,7 +380,8 @@ chw_status host_impl(const void* in_host, void* out_host, chw_dtype dtype, int64
     DeviceState& s = d;
     if (s.ws_bytes < 2 * ws_chunk) {
       if (s.ws) {
-        cudaDeviceSynchronize();
+        // Only host calls (serialised by s.mu) use s.ws; drain their streams.
+        for (int i = 0; i < 2; ++i) cudaStreamSynchronize(s.streams[i]);
         cudaFree(s.ws);
       }
       s.ws = nullptr;
@@ -490,17 +550,11 @@ chw_status chw_b200_haar_forward(const void* in, void* out, chw_dtype dtype, int
   if (batch == 0) return CHW_OK;
   if (!in || !out) return fail(CHW_ERR_ARGUMENT, "haar_forward: null buffer");
   const size_t need = haar_workspace_bytes(dtype, batch, n);
-  void* ws = workspace;
-  if (need > 0) {
-    if (ws == nullptr) {
-      int dev = 0;
-      if (chw_status s = current_device(&dev)) return s;
-      if (chw_status s = ensure_workspace(dev, need, &ws)) return s;
-    } else if (workspace_bytes < need) {
-      return fail(CHW_ERR_WORKSPACE, "haar_forward: workspace too small");
-    }
-  }
-  return haar_forward_device(in, out, dtype, batch, n, mode, ws, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (chw_status s = check_aligned("haar_forward", in, out, need ? workspace : nullptr)) return s;
+  WsLease lease;
+  if (chw_status s = lease_workspace("haar_forward", need, workspace, workspace_bytes, st, &lease)) return s;
+  return haar_forward_device(in, out, dtype, batch, n, mode, lease.p, st);
 }
 
 chw_status chw_b200_haar_forward_host(const void* in_host, void* out_host, chw_dtype dtype, int64_t batch,
@@ -543,15 +597,11 @@ chw_status chw_b200_haar_inverse(const void* in, void* out, chw_dtype dtype, int
   if (batch == 0) return CHW_OK;
   if (!in || !out) return fail(CHW_ERR_ARGUMENT, "haar_inverse: null buffer");
   const size_t need = haar_inverse_workspace_bytes(dtype, batch, n);
-  void* ws = workspace;
-  if (ws == nullptr) {
-    int dev = 0;
-    if (chw_status s = current_device(&dev)) return s;
-    if (chw_status s = ensure_workspace(dev, need, &ws)) return s;
-  } else if (workspace_bytes < need) {
-    return fail(CHW_ERR_WORKSPACE, "haar_inverse: workspace too small");
-  }
-  return haar_inverse_device(in, out, dtype, batch, n, mode, ws, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (chw_status s = check_aligned("haar_inverse", in, out, workspace)) return s;
+  WsLease lease;
+  if (chw_status s = lease_workspace("haar_inverse", need, workspace, workspace_bytes, st, &lease)) return s;
+  return haar_inverse_device(in, out, dtype, batch, n, mode, lease.p, st);
 }
 
 chw_status chw_b200_haar_walsh_forward(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
@@ -562,6 +612,7 @@ chw_status chw_b200_haar_walsh_forward(const void* in, void* out, chw_dtype dtyp
   if (batch == 0) return CHW_OK;
   if (!in || !out) return fail(CHW_ERR_ARGUMENT, "haar_walsh_forward: null buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (chw_status s = check_aligned("haar_walsh_forward", in, out, nullptr)) return s;
   const size_t es = elem_size(dtype);
   if (in != out) CHW_CUDA(cudaMemcpyAsync(out, in, (size_t)batch * n * es, cudaMemcpyDeviceToDevice, st));
   const int m = level_of(n);
@@ -569,13 +620,12 @@ chw_status chw_b200_haar_walsh_forward(const void* in, void* out, chw_dtype dtyp
   // Gather block j of every row into a contiguous [batch][2^j] buffer, run the
   // batched dyadic kernel on it, scatter back.
   const size_t tmp_bytes = (size_t)batch * (n / 2) * es;
-  int dev = 0;
-  if (chw_status s = current_device(&dev)) return s;
   size_t inner = 0;
   for (int j = 1; j <= m - 1; ++j) inner = std::max(inner, workspace_for(dtype, batch, j));
-  void* ws = nullptr;
-  if (chw_status s = ensure_workspace(dev, align256(tmp_bytes) + inner, &ws)) return s;
-  char* tmp = static_cast<char*>(ws);
+  WsLease lease;
+  if (chw_status s = lease_workspace("haar_walsh_forward", align256(tmp_bytes) + inner, nullptr, 0, st, &lease))
+    return s;
+  char* tmp = static_cast<char*>(lease.p);
   void* inner_ws = tmp + align256(tmp_bytes);
   char* o = static_cast<char*>(out);
   for (int j = 1; j <= m - 1; ++j) {

@@ -55,6 +55,97 @@ inline chw_status check_launch(const char* what) {
   return CHW_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Persisting-L2 window for an L2-resident intermediate (the multi-phase
+// schedules' workspace).  B200 sets aside up to
+// cudaDevAttrMaxPersistingL2CacheSize (79 MiB measured) of the 126 MB L2 for
+// "persisting" lines, which normal (streaming) lines cannot evict.  The
+// launches that touch the workspace carry an access-policy window over it
+// (hitProp Persisting, missProp Streaming) so the intermediate's lines stay
+// in L2 while the input and output stream past, and are overwritten there
+// instead of being written back.  OFF by default (CHW_B200_L2PERSIST=1 turns
+// it on for A/B runs): measured, a carve-out with a 1 GiB window (K4T, 16-row
+// chunks, hitRatio 0.08) cut cfg5 from 0.43 to 0.16 of HBM peak AND the same
+// process's plain 1 GiB copy from 6.2 to 2.9 TB/s; a 1-row window (K4T,
+// chunk 1) ran 272 vs 299 Gelem/s without it; K6 (cfg4, 37 MiB window)
+// gained ~1.5 %.  DESIGN.md §4.3.
+// ---------------------------------------------------------------------------
+inline int l2_persist_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("CHW_B200_L2PERSIST");
+    return (e && e[0] >= '0' && e[0] <= '9') ? e[0] - '0' : 0;
+  }();
+  return v;
+}
+// Raise the device's persisting carve-out to at least `bytes` (capped at the
+// device maximum) once; returns the carve-out in effect (0 = unavailable).
+inline size_t ensure_persist_carveout(size_t bytes) {
+  static std::atomic<size_t> have[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return 0;
+  }
+  size_t cur = have[dev].load(std::memory_order_acquire);
+  if (cur >= bytes) return cur;
+  int maxp = 0;
+  if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess || maxp <= 0) {
+    cudaGetLastError();
+    return 0;
+  }
+  const size_t want = std::min<size_t>(bytes, (size_t)maxp);
+  size_t now = 0;
+  if (cudaDeviceGetLimit(&now, cudaLimitPersistingL2CacheSize) == cudaSuccess && now >= want) {
+    have[dev].store(now, std::memory_order_release);
+    return now;
+  }
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  have[dev].store(want, std::memory_order_release);
+  return want;
+}
+// Launch attribute list: an access-policy window over [base, base+bytes)
+// when persistence is on and available, else none.
+struct PersistWindow {
+  cudaLaunchAttribute attr[1];
+  unsigned n = 0;
+  PersistWindow(const void* base, size_t bytes) {
+    if (!l2_persist_mode() || !base || bytes == 0) return;
+    const size_t carve = ensure_persist_carveout(bytes);
+    if (carve == 0) return;
+    int dev = 0, maxw = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess || maxw <= 0) {
+      cudaGetLastError();
+      return;
+    }
+    const size_t win = std::min<size_t>(bytes, (size_t)maxw);
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    attr[0].val.accessPolicyWindow.num_bytes = win;
+    attr[0].val.accessPolicyWindow.hitRatio = std::min(1.0f, (float)((double)carve / (double)win));
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    n = 1;
+  }
+};
+template <class... KArgs, class... Args>
+chw_status launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     const PersistWindow& w, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = const_cast<cudaLaunchAttribute*>(w.attr);
+  cfg.numAttrs = w.n;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelEx");
+  return CHW_OK;
+}
+
 template <auto Kern>
 chw_status prep_kernel(int smem) {
   // One-time (per kernel, per device) opt-in above 48 KiB of dynamic shared memory.
@@ -492,7 +583,10 @@ chw_status launch_rowpipe_ws4_m16_x(const float* in, float* out, void* ws, int64
   const int grid = (int)std::min<int64_t>(batch, (int64_t)sms);
   TmapParam t0, t1;
   if (chw_status s = rowpipe_tmaps(ws, grid, &t0, &t1)) return s;
-  k<<<grid, 4 * P::NT + 64, smem, st>>>(in, out, static_cast<float*>(ws), (uint64_t)batch, scale, t0, t1);
+  const PersistWindow win(ws, (size_t)grid << 18);  // one 256 KiB workspace row per CTA
+  if (chw_status s = launch_ex(k, grid, 4 * P::NT + 64, smem, st, win, in, out, static_cast<float*>(ws),
+                               (uint64_t)batch, scale, t0, t1))
+    return s;
   return check_launch("rowpipe_ws4_kernel");
 }
 
@@ -519,6 +613,15 @@ chw_status launch_rowpipe_m16(const float* in, float* out, void* ws, int64_t bat
 // kernel.  Measured: 38.5 % of HBM peak vs 31 % for the
 // one-launch dataflow schedule, whose dependency waits drain the pipelines.
 constexpr int64_t kM24Chunk = 16;  // rows per chunk: 1 GiB intermediate
+// K4T rows per chunk (CHW_B200_M24_CHUNK=1..16; default 16).
+inline int64_t m24_chunk_rows() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("CHW_B200_M24_CHUNK");
+    const long x = e ? std::strtol(e, nullptr, 10) : 0;
+    return (int64_t)((x >= 1 && x <= kM24Chunk) ? x : kM24Chunk);
+  }();
+  return v;
+}
 template <bool SCALE>
 chw_status launch_two_pass_m24(const float* in, float* out, void* ws, int64_t batch, float scale,
                                cudaStream_t st) {
@@ -587,15 +690,21 @@ chw_status launch_two_pass_tma_m24(const float* in, float* out, void* ws, int64_
   CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   float* mid = static_cast<float*>(ws);
   TmapParam none{};
-  for (int64_t r0 = 0; r0 < batch; r0 += kM24Chunk) {
-    const int64_t rows = std::min<int64_t>(kM24Chunk, batch - r0);
+  const int64_t chunk = m24_chunk_rows();
+  const PersistWindow win(mid, (size_t)std::min<int64_t>(chunk, batch) << 26);
+  for (int64_t r0 = 0; r0 < batch; r0 += chunk) {
+    const int64_t rows = std::min<int64_t>(chunk, batch - r0);
     const uint64_t items = (uint64_t)rows * 1024;
     const unsigned grid = (unsigned)std::min<uint64_t>(items, (uint64_t)sms);
-    ka<<<grid, P::NT + 32, smem, st>>>(in + ((uint64_t)r0 << 24), mid, items, scale, none);
+    if (chw_status s = launch_ex(ka, grid, P::NT + 32, smem, st, win, in + ((uint64_t)r0 << 24), mid, items, scale,
+                                 none))
+      return s;
     if (chw_status s = check_launch("pass_tma_kernel(A)")) return s;
     TmapParam tm;
     if (chw_status s = m24_mid_tmap(mid, rows, &tm)) return s;
-    kb<<<grid, P::NT + 32, smem, st>>>(mid, out + ((uint64_t)r0 << 24), items, scale, tm);
+    if (chw_status s = launch_ex(kb, grid, P::NT + 32, smem, st, win, (const float*)mid,
+                                 out + ((uint64_t)r0 << 24), items, scale, tm))
+      return s;
     if (chw_status s = check_launch("pass_tma_kernel(B)")) return s;
   }
   return CHW_OK;

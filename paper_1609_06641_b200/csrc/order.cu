@@ -96,8 +96,10 @@ chw_status permute_typed(const void* src, void* dst, chw_order order, int64_t ba
   const uint64_t rows = (uint64_t)batch;
   if (order == CHW_ORDER_NATURAL && m >= 10) {
     const uint64_t tiles = rows << (m - 10);
-    for (uint64_t t0 = 0; t0 < tiles; t0 += 0x7fffffffull) {
-      const unsigned g = (unsigned)std::min<uint64_t>(tiles - t0, 0x7fffffffull);
+    // Grid splits advance by a whole number of rows (tiles are row-major).
+    const uint64_t step = (0x7fffffffull >> (m - 10)) << (m - 10);
+    for (uint64_t t0 = 0; t0 < tiles; t0 += step) {
+      const unsigned g = (unsigned)std::min<uint64_t>(tiles - t0, step);
       // Offset by whole rows only: tiles are row-major, so t0 is row-aligned here.
       const uint64_t row0 = t0 >> (m - 10);
       rev_tiled_kernel<E><<<g, dim3(32, 8), 0, st>>>(s + (row0 << m), d + (row0 << m), m, rows - row0);

@@ -1,0 +1,126 @@
+"""Full-size parity at the BASELINE.json batch sizes (slow): the CUDA path on
+the stated batch of every config, compared with the REFERENCE compiled from
+/root/reference (oracle/_ref; the C port where the reference was not built)
+on the same input bytes.
+
+* cfg1-cfg4: every row of the stated batch; f64 bit-exact, f32 relative L2
+  <= 1e-5 per row, bf16 <= 1e-2 per row (north_star tolerances), plus the
+  exact integer order probe on every row (Unnormalized, integer inputs whose
+  partial sums are all exact: a wrong permutation cannot pass).
+* cfg5 (256 x 2^24, 16 GiB in + 16 GiB out): the full batch runs on the GPU;
+  32 rows spread over all 16 row chunks of the m = 24 schedule (two per chunk,
+  first and last row of each) are checked, and the order probe likewise.
+
+Follows the reference's own tests (transforms_test.cpp:123-132 CHW == dense
+dyadic, exact in int64; :241-248 orthonormal agreement).
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+BACKEND = "reference" if oracle.have_reference() else "port"
+TOL = {"f64": 1e-12, "f32": 1e-5, "bf16": 1e-2}
+CFGS = {
+    # name: (dtype, rows, m, dist)
+    "cfg1": ("f64", 1024, 10, "uniform"),
+    "cfg2": ("f32", 65536, 12, "normal"),
+    "cfg3": ("bf16", 1 << 20, 7, "normal"),
+    "cfg4": ("f32", 4096, 16, "uniform"),
+    "cfg5": ("f32", 256, 24, "normal"),
+}
+
+
+def _tdt(torch, dt):
+    return {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dt]
+
+
+def _make(torch, cuda, dt, rows, m, dist, seed):
+    g = torch.Generator(device=cuda)
+    g.manual_seed(seed)
+    wide = torch.float64 if dt == "f64" else torch.float32
+    if dist == "normal":
+        x = torch.randn(rows, 1 << m, generator=g, device=cuda, dtype=wide)
+    else:
+        x = torch.rand(rows, 1 << m, generator=g, device=cuda, dtype=wide) * 2 - 1
+    return x.to(_tdt(torch, dt)).contiguous()
+
+
+def _rows_to_check(cfg, rows):
+    if cfg != "cfg5":
+        return None  # all rows
+    idx = []
+    for c in range(16):  # 16-row chunks: first and last row of each
+        idx += [16 * c, 16 * c + 15]
+    return idx
+
+
+def _check_rows(x_rows, y_rows, dt):
+    """Per-row relative L2 of y against the reference on x (float64 arrays)."""
+    ref = oracle.chw_batch(x_rows, oracle.ORTHONORMAL, backend=BACKEND, threads=0)
+    if dt == "f64":
+        assert np.array_equal(y_rows.view(np.uint64), ref.view(np.uint64)), "f64 not bit-exact"
+    err = np.linalg.norm(y_rows - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-300)
+    return float(err.max())
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_fullsize_orthonormal_vs_reference(cuda, cfg):
+    import torch
+
+    import paper_1609_06641_b200 as chw
+
+    dt, rows, m, dist = CFGS[cfg]
+    x = _make(torch, cuda, dt, rows, m, dist, 1609 + rows)
+    out = torch.empty_like(x)
+    chw.chw_forward_batched_(x, chw.ScalingMode.Orthonormal, out=out)
+    torch.cuda.synchronize()
+    idx = _rows_to_check(cfg, rows)
+    if idx is None:
+        # in slices, to bound host memory (f64 copies of 2^28 elements)
+        worst = 0.0
+        step = max(1, (1 << 26) >> m)
+        for r0 in range(0, rows, step):
+            xs = x[r0:r0 + step].to(torch.float64).cpu().numpy()
+            ys = out[r0:r0 + step].to(torch.float64).cpu().numpy()
+            worst = max(worst, _check_rows(xs, ys, dt))
+    else:
+        it = torch.tensor(idx, device=cuda)
+        worst = 0.0
+        for k in range(0, len(idx), 8):
+            sub = it[k:k + 8]
+            xs = x.index_select(0, sub).to(torch.float64).cpu().numpy()
+            ys = out.index_select(0, sub).to(torch.float64).cpu().numpy()
+            worst = max(worst, _check_rows(xs, ys, dt))
+    assert worst <= TOL[dt], f"{cfg}: max relative L2 {worst}"
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_fullsize_exact_order_probe(cuda, cfg):
+    """Unnormalized on integer inputs with exact partial sums must equal the
+    int64 reference bit for bit on every checked row: the index permutation
+    (dyadic order) is verified exactly at the stated batch size."""
+    import torch
+
+    import paper_1609_06641_b200 as chw
+
+    dt, rows, m, _ = CFGS[cfg]
+    bound = {"f32": 1 << max(0, 24 - m), "bf16": 1, "f64": 1 << 20}[dt]
+    g = torch.Generator(device=cuda)
+    g.manual_seed(4242 + m)
+    xi = torch.randint(-bound, bound + 1, (rows, 1 << m), generator=g, device=cuda, dtype=torch.int64)
+    x = xi.to(_tdt(torch, dt))
+    chw.chw_forward_batched_(x, chw.ScalingMode.Unnormalized)
+    torch.cuda.synchronize()
+    idx = _rows_to_check(cfg, rows)
+    step = max(1, (1 << 26) >> m)
+    chunks = [list(range(r0, min(rows, r0 + step))) for r0 in range(0, rows, step)] if idx is None \
+        else [idx[k:k + 8] for k in range(0, len(idx), 8)]
+    for sub in chunks:
+        it = torch.tensor(sub, device=cuda)
+        xs = xi.index_select(0, it).cpu().numpy()
+        got = x.index_select(0, it).to(torch.float64).cpu().numpy()
+        want = oracle.chw_batch(xs, oracle.UNNORMALIZED, backend=BACKEND, threads=0)
+        assert np.array_equal(got, want.astype(np.float64)), f"{cfg}: order probe mismatch in rows {sub[0]}.."

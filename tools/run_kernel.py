@@ -27,7 +27,7 @@ def main():
     name, dt, rows, m, _ = bench.CONFIGS[args.config]
     rows = args.rows or rows
     dev = torch.device("cuda:0")
-    x = bench.make_input(torch, args.config, rows, dev, 0)
+    x = bench.make_input(torch, args.config, 0, rows, dev)
     out = torch.empty_like(x)
     mode = chw.ScalingMode.Orthonormal if args.mode == "ortho" else chw.ScalingMode.Unnormalized
     for _ in range(args.reps):
