@@ -42,7 +42,6 @@ size_t elem_size(chw_dtype d) {
   }
   return 0;
 }
-size_t inter_size(chw_dtype d) { return d == CHW_BF16 ? 4 : elem_size(d); }
 
 }  // namespace
 

@@ -25,6 +25,7 @@
 
 #include <cstdint>
 #include <type_traits>
+#include <utility>
 #include <cuda_bf16.h>
 
 #define CHW_HD __host__ __device__ __forceinline__
@@ -49,6 +50,20 @@ struct Cat {
   static constexpr int N = A::N + B::N;
   CHW_HD static constexpr int at(int k) { return k < A::N ? A::at(k) : B::at(k - A::N); }
 };
+
+// Compile-time loop: f(std::integral_constant<int, I>) for I = 0..N-1.  The
+// register-indexed loops below use it so every per-register offset is a C++
+// constant expression (folded by the front end) instead of an unrolled loop
+// that NVVM has to simplify — E = 128 tiles compile an order of magnitude
+// faster this way.
+template <class F, int... I>
+__device__ __forceinline__ void static_for_impl(F& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 template <class L>
 CHW_HD constexpr int find(int v) {
@@ -490,20 +505,31 @@ __device__ __forceinline__ void bf2(float& a0, float& a1, float& b0, float& b1) 
 // packed FADD2 instructions: half the FP issue slots, identical results.
 template <class L, class Bits, bool PER_STAGE, class C>
 __device__ __forceinline__ void butterflies(C (&v)[L::E]) {
-#pragma unroll
-  for (int i = 0; i < Bits::N; ++i) {
-    const int k = L::slot(Bits::at(i));
-    if constexpr (std::is_same<C, float>::value && !PER_STAGE && L::E >= 4) {
-      if (k > 0) {
-#pragma unroll
-        for (int r = 0; r < L::E; r += 2)
-          if (!((r >> k) & 1)) bf2(v[r], v[r | 1], v[r | (1 << k)], v[(r | (1 << k)) | 1]);
-        continue;
+  if constexpr (std::is_same<C, float>::value && !PER_STAGE && L::E >= 4) {
+    static_for<Bits::N>([&](auto I) {
+      constexpr int k = L::slot(Bits::at(decltype(I)::value));
+      static_assert(k >= 0, "butterfly bit must be a register bit");
+      if constexpr (k > 0) {
+        static_for<L::E / 2>([&](auto H) {
+          constexpr int r = 2 * decltype(H)::value;
+          if constexpr (!((r >> k) & 1)) bf2(v[r], v[r | 1], v[r | (1 << k)], v[(r | (1 << k)) | 1]);
+        });
+      } else {
+        static_for<L::E>([&](auto R) {
+          constexpr int r = decltype(R)::value;
+          if constexpr (!((r >> k) & 1)) bf<PER_STAGE>(v[r], v[r | (1 << k)]);
+        });
       }
-    }
-#pragma unroll
-    for (int r = 0; r < L::E; ++r)
-      if (!((r >> k) & 1)) bf<PER_STAGE>(v[r], v[r | (1 << k)]);
+    });
+  } else {
+    static_for<Bits::N>([&](auto I) {
+      constexpr int k = L::slot(Bits::at(decltype(I)::value));
+      static_assert(k >= 0, "butterfly bit must be a register bit");
+      static_for<L::E>([&](auto R) {
+        constexpr int r = decltype(R)::value;
+        if constexpr (!((r >> k) & 1)) bf<PER_STAGE>(v[r], v[r | (1 << k)]);
+      });
+    });
   }
 }
 
@@ -532,14 +558,18 @@ template <class L, class Map, Cache CO = Cache::kNC, class T, class C>
 __device__ __forceinline__ void load_global(const T* __restrict__ base, C (&v)[L::E], uint32_t tid) {
   constexpr int VB = vec_bits<L, Map>(IoTraits<T>::VMAX);
   const uint32_t tb = thr_off<L, Map>(tid);
-#pragma unroll
-  for (int r = 0; r < L::E; ++r) {
-    if (!vec_head<L, Map>(r, VB)) continue;
-    C tmp[1 << VB];
-    VecIO<T, VB, CO>::ld(base + (tb + reg_off<L, Map>(r)), tmp);
-#pragma unroll
-    for (int q = 0; q < (1 << VB); ++q) v[vec_elem<L, Map>(r, q, VB)] = tmp[q];
-  }
+  static_for<L::E>([&](auto R) {
+    constexpr int r = decltype(R)::value;
+    if constexpr (vec_head<L, Map>(r, VB)) {
+      constexpr uint32_t ro = reg_off<L, Map>(r);
+      C tmp[1 << VB];
+      VecIO<T, VB, CO>::ld(base + (tb + ro), tmp);
+      static_for<(1 << VB)>([&](auto Q) {
+        constexpr int q = decltype(Q)::value;
+        v[vec_elem<L, Map>(r, q, VB)] = tmp[q];
+      });
+    }
+  });
 }
 
 // Predicated variant for a partial last tile: element valid iff its offset < limit.
@@ -570,17 +600,19 @@ __device__ __forceinline__ void store_global(T* __restrict__ base, const C (&v)[
                                              C scale) {
   constexpr int VB = vec_bits<L, Map>(IoTraits<T>::VMAX);
   const uint32_t tb = thr_off<L, Map>(tid);
-#pragma unroll
-  for (int r = 0; r < L::E; ++r) {
-    if (!vec_head<L, Map>(r, VB)) continue;
-    C tmp[1 << VB];
-#pragma unroll
-    for (int q = 0; q < (1 << VB); ++q) {
-      const C x = v[vec_elem<L, Map>(r, q, VB)];
-      tmp[q] = SCALE ? x * scale : x;
+  static_for<L::E>([&](auto R) {
+    constexpr int r = decltype(R)::value;
+    if constexpr (vec_head<L, Map>(r, VB)) {
+      constexpr uint32_t ro = reg_off<L, Map>(r);
+      C tmp[1 << VB];
+      static_for<(1 << VB)>([&](auto Q) {
+        constexpr int q = decltype(Q)::value;
+        const C x = v[vec_elem<L, Map>(r, q, VB)];
+        tmp[q] = SCALE ? x * scale : x;
+      });
+      VecIO<T, VB, CO>::st(base + (tb + ro), tmp);
     }
-    VecIO<T, VB, CO>::st(base + (tb + reg_off<L, Map>(r)), tmp);
-  }
+  });
 }
 
 template <class L, class Map, bool SCALE, class T, class C>
@@ -628,16 +660,19 @@ __device__ __forceinline__ void smem_store(C* sm, const C (&v)[L::E], uint32_t t
   constexpr int VB = smem_vec_bits<L, S, SmemCap<C>::V>();
   constexpr uint32_t tmask = S::image(thr_mask<L, IdMap>());
   const uint32_t sb = S::apply(thr_off<L, IdMap>(tid));
-#pragma unroll
-  for (int r = 0; r < L::E; ++r) {
-    if (!vec_head<L, IdMap>(r, VB)) continue;
-    const uint32_t so = S::apply(reg_off<L, IdMap>(r));
-    const uint32_t a = (so & tmask) ? (sb ^ so) : (sb + so);
-    C tmp[1 << VB];
-#pragma unroll
-    for (int q = 0; q < (1 << VB); ++q) tmp[q] = v[vec_elem<L, IdMap>(r, q, VB)];
-    SmemVec<C, VB>::st(sm + a, tmp);
-  }
+  static_for<L::E>([&](auto R) {
+    constexpr int r = decltype(R)::value;
+    if constexpr (vec_head<L, IdMap>(r, VB)) {
+      constexpr uint32_t so = S::apply(reg_off<L, IdMap>(r));
+      const uint32_t a = (so & tmask) ? (sb ^ so) : (sb + so);
+      C tmp[1 << VB];
+      static_for<(1 << VB)>([&](auto Q) {
+        constexpr int q = decltype(Q)::value;
+        tmp[q] = v[vec_elem<L, IdMap>(r, q, VB)];
+      });
+      SmemVec<C, VB>::st(sm + a, tmp);
+    }
+  });
 }
 
 template <class L, class S, class C>
@@ -645,16 +680,19 @@ __device__ __forceinline__ void smem_load(const C* sm, C (&v)[L::E], uint32_t ti
   constexpr int VB = smem_vec_bits<L, S, SmemCap<C>::V>();
   constexpr uint32_t tmask = S::image(thr_mask<L, IdMap>());
   const uint32_t sb = S::apply(thr_off<L, IdMap>(tid));
-#pragma unroll
-  for (int r = 0; r < L::E; ++r) {
-    if (!vec_head<L, IdMap>(r, VB)) continue;
-    const uint32_t so = S::apply(reg_off<L, IdMap>(r));
-    const uint32_t a = (so & tmask) ? (sb ^ so) : (sb + so);
-    C tmp[1 << VB];
-    SmemVec<C, VB>::ld(sm + a, tmp);
-#pragma unroll
-    for (int q = 0; q < (1 << VB); ++q) v[vec_elem<L, IdMap>(r, q, VB)] = tmp[q];
-  }
+  static_for<L::E>([&](auto R) {
+    constexpr int r = decltype(R)::value;
+    if constexpr (vec_head<L, IdMap>(r, VB)) {
+      constexpr uint32_t so = S::apply(reg_off<L, IdMap>(r));
+      const uint32_t a = (so & tmask) ? (sb ^ so) : (sb + so);
+      C tmp[1 << VB];
+      SmemVec<C, VB>::ld(sm + a, tmp);
+      static_for<(1 << VB)>([&](auto Q) {
+        constexpr int q = decltype(Q)::value;
+        v[vec_elem<L, IdMap>(r, q, VB)] = tmp[q];
+      });
+    }
+  });
 }
 
 }  // namespace chwb

@@ -272,105 +272,4 @@ struct FusedF32M24 {
   }
 };
 
-struct FusedGeom {
-  uint32_t nchunks;     // row chunks
-  uint32_t nA, nB;      // tiles per chunk
-  uint32_t lag, nslots;
-  uint32_t chunk_rows;  // rows per chunk (last chunk may be shorter: rows_last)
-  uint32_t rows_last;
-};
-
-// Work item w -> (is_a, chunk, tile).  Order: for rounds t = 0, 1, ...: the A
-// tiles of chunk t (if t < nchunks), then the B tiles of chunk t - lag (if
-// 0 <= t - lag < nchunks).  Rounds 0..lag-1 hold only A tiles, the last lag
-// rounds only B tiles.
-__device__ __forceinline__ bool decode_work(uint32_t w, const FusedGeom& g, bool& is_a, uint32_t& q,
-                                            uint32_t& tile) {
-  const uint32_t per = g.nA + g.nB;
-  const uint32_t lag = g.lag < g.nchunks ? g.lag : g.nchunks;
-  const uint32_t head = lag * g.nA;  // rounds 0..lag-1
-  if (w < head) {
-    is_a = true;
-    q = w / g.nA;
-    tile = w - q * g.nA;
-    return true;
-  }
-  const uint32_t w2 = w - head;
-  const uint32_t mid_rounds = g.nchunks - lag;  // rounds lag..nchunks-1: A(t), B(t-lag)
-  if (w2 < mid_rounds * per) {
-    const uint32_t r = w2 / per;
-    const uint32_t off = w2 - r * per;
-    is_a = off < g.nA;
-    q = is_a ? (lag + r) : r;
-    tile = is_a ? off : off - g.nA;
-    return true;
-  }
-  const uint32_t w3 = w2 - mid_rounds * per;  // tail rounds: B of the last `lag` chunks
-  if (w3 < lag * g.nB) {
-    is_a = false;
-    q = mid_rounds + w3 / g.nB;
-    tile = w3 - (w3 / g.nB) * g.nB;
-    return true;
-  }
-  return false;
-}
-
-// ctr[0] = work counter, ctr[1 .. nchunks] = A done, ctr[1+nchunks ..] = B done.
-template <class F, bool SCALE>
-__global__ void __launch_bounds__(F::NT, F::MIN_BLOCKS) fused_kernel(const typename F::T* __restrict__ in,
-                                                      typename F::T* __restrict__ out,
-                                                      typename F::W* __restrict__ slots,
-                                                      uint32_t* __restrict__ ctr, FusedGeom g,
-                                                      typename F::W scale) {
-  using W = typename F::W;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  W* sm = reinterpret_cast<W*>(smem_raw);
-  __shared__ uint32_t s_work;
-  uint32_t* a_done = ctr + 1;
-  uint32_t* b_done = ctr + 1 + g.nchunks;
-  constexpr uint64_t n = 1ull << F::M;
-  const uint64_t slot_elems = (uint64_t)g.chunk_rows << F::M;
-  // One barrier per item before the tile (claim + dependency poll by thread 0)
-  // and one after it (then thread 0 publishes completion with red.release).
-  for (;;) {
-    if (threadIdx.x == 0) {
-      const uint32_t w0 = atomicAdd(ctr, 1u);
-      bool a0;
-      uint32_t q0, t0;
-      if (decode_work(w0, g, a0, q0, t0)) {
-        if (a0) {
-          if (q0 >= g.nslots) wait_at_least(&b_done[q0 - g.nslots], g.nB);
-        } else {
-          wait_at_least(&a_done[q0], g.nA);
-        }
-      }
-      s_work = w0;
-    }
-    __syncthreads();
-    const uint32_t w = s_work;
-    bool is_a;
-    uint32_t q, tile;
-    if (!decode_work(w, g, is_a, q, tile)) break;
-    const uint32_t rows_q = (q == g.nchunks - 1) ? g.rows_last : g.chunk_rows;
-    W* slot = slots + (uint64_t)(q % g.nslots) * slot_elems;
-    if (is_a) {
-      uint32_t row, in_off, mid_off;
-      F::a_offsets(tile, row, in_off, mid_off);
-      if (row < rows_q) {
-        const uint64_t grow = (uint64_t)q * g.chunk_rows + row;
-        F::template run_a<SCALE>(in + grow * n + in_off, slot + (uint64_t)row * n + mid_off, sm, scale);
-      }
-    } else {
-      uint32_t row, mid_off, out_off;
-      F::b_offsets(tile, row, mid_off, out_off);
-      if (row < rows_q) {
-        const uint64_t grow = (uint64_t)q * g.chunk_rows + row;
-        F::template run_b<SCALE>(slot + (uint64_t)row * n + mid_off, out + grow * n + out_off, sm, scale);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) red_release_add(is_a ? &a_done[q] : &b_done[q], 1u);
-  }
-}
-
 }  // namespace chwb

@@ -12,41 +12,6 @@
 
 namespace chwb {
 
-// bf16 m = 7 (cfg3) item: PlanBF16M7's layouts (plans.cuh) with the tile
-// (32 rows x 128, 8 KiB) read from a bf16 stage in natural order: 8 values
-// (tile bits 0..2) per 16-byte LDS, converted to fp32 in registers.
-struct ItemBF16M7 {
-  using P = PlanBF16M7;
-  using IO = __nv_bfloat16;
-  static constexpr int TILE = 1 << P::kTB;
-  static constexpr int E = P::L0::E;
-  using L0 = P::L0;
-  __device__ __forceinline__ static void phase0(const IO* stage, float* work, float (&v)[E], uint32_t tid) {
-    constexpr int VB = 3;
-    static_assert(vec_bits<L0, IdMap>(VB) == VB, "8 consecutive bf16 per thread vector");
-    const uint32_t tb = thr_off<L0, IdMap>(tid);
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-      if (!vec_head<L0, IdMap>(r, VB)) continue;
-      const uint4 w = *reinterpret_cast<const uint4*>(stage + tb + reg_off<L0, IdMap>(r));
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        v[vec_elem<L0, IdMap>(r, 2 * q, VB)] = __uint_as_float(ws[q] << 16);
-        v[vec_elem<L0, IdMap>(r, 2 * q + 1, VB)] = __uint_as_float(ws[q] & 0xffff0000u);
-      }
-    }
-    butterflies<L0, BL<0, 1, 2, 6>, false>(v);
-    smem_store<L0, P::S>(work, v, tid);
-  }
-  template <bool SCALE>
-  __device__ __forceinline__ static void phase1(const float* work, IO* gout, float (&v)[E], uint32_t tid,
-                                                float scale) {
-    smem_load<P::L1, P::S>(work, v, tid);
-    butterflies<P::L1, BL<3, 4, 5>, false>(v);
-    store_global<P::L1, RevMap<7>, SCALE, Cache::kStream>(gout, v, tid, scale);
-  }
-};
 // f32 m = 12 item adapter (K1P's TwoPhase item).
 struct ItemF32M12 {
   using T = PipeF32M12::Item;

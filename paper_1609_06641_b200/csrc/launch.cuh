@@ -17,8 +17,6 @@
 #include "chw_kernels.cuh"
 #include "fused.cuh"
 #include "pipelined.cuh"
-#include "warpspec.cuh"
-#include "cluster.cuh"
 #include "rowpipe.cuh"
 #include "k1t.cuh"
 #include "passtma.cuh"
@@ -38,15 +36,6 @@ void count_launch();
     cudaError_t e_ = (call);                            \
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
-
-// A/B switch for the pipelined kernels (CHW_B200_PIPELINE=0 disables them).
-inline bool pipeline_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("CHW_B200_PIPELINE");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
 
 inline chw_status check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -162,37 +151,10 @@ chw_status prep_kernel(int smem) {
   return CHW_OK;
 }
 
-template <class P, bool SCALE>
-chw_status launch_k1p(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
-  constexpr auto k = k1p_kernel<P, SCALE>;
-  if (chw_status s = prep_kernel<k>(P::SMEM_BYTES)) return s;
-  static int occ_cache[64] = {0};
-  static int sms_cache[64] = {0};
-  int dev = 0;
-  if (chw_status s = current_device(&dev)) return s;
-  if (occ_cache[dev] == 0) {
-    int occ = 0, sms = 0;
-    CHW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, P::NT, P::SMEM_BYTES));
-    CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    occ_cache[dev] = std::max(1, occ);
-    sms_cache[dev] = sms;
-  }
-  const uint64_t tiles = (uint64_t)batch;  // one row per tile
-  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)occ_cache[dev] * sms_cache[dev]);
-  k<<<grid, P::NT, P::SMEM_BYTES, st>>>(in, out, tiles, scale);
-  return check_launch("k1p_kernel");
-}
-
-// K1T (k1t.cuh): TMA-fed single-pass kernel for f32 m = 12 (cfg2, default).
-// CHW_B200_K1T=0 selects K1P, 1..4 the (stages, groups) variants below.
-// Same-box A/B: variant 2 95.3-95.9 % vs K1P 90.7-91.2 %.
-inline int k1t_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("CHW_B200_K1T");
-    return (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 2;
-  }();
-  return v;
-}
+// K1T (k1t.cuh): TMA-fed single-pass kernel for f32 m = 12 (cfg2, default):
+// 8-stage ring, 2 compute groups.  Same-box A/B: 95.3-95.9 %
+// of HBM peak vs 90.7-91.2 % for the cp.async K1P it replaced (removed, with
+// the other measured ring/group variants, in round 2).
 template <class Item, int TB, int S, int NG, bool SCALE>
 chw_status launch_k1t_x(const typename Item::IO* in, typename Item::IO* out, int64_t tiles, float scale,
                         cudaStream_t st) {
@@ -210,34 +172,7 @@ chw_status launch_k1t_x(const typename Item::IO* in, typename Item::IO* out, int
 }
 template <bool SCALE>
 chw_status launch_k1t(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
-  switch (k1t_variant()) {
-    case 1: return launch_k1t_x<ItemF32M12, 12, 8, 4, SCALE>(in, out, batch, scale, st);
-    case 3: return launch_k1t_x<ItemF32M12, 12, 9, 3, SCALE>(in, out, batch, scale, st);
-    case 4: return launch_k1t_x<ItemF32M12, 12, 10, 2, SCALE>(in, out, batch, scale, st);
-    default: return launch_k1t_x<ItemF32M12, 12, 8, 2, SCALE>(in, out, batch, scale, st);
-  }
-}
-// bf16 m = 7 (cfg3): CHW_B200_K1T_BF16=1..3 selects the TMA-fed kernel
-// (tiles of 32 rows; the batch remainder goes through the K1 kernel).  Off by
-// default: same-box A/B 84.7-87.8 % (variant 2) vs K1 84.9-85.2 %, the 256-
-// thread bf16 item allows at most 3 groups per CTA.
-inline int k1t_bf16_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("CHW_B200_K1T_BF16");
-    return (e && e[0] >= '0' && e[0] <= '5') ? e[0] - '0' : 0;
-  }();
-  return v;
-}
-template <bool SCALE>
-chw_status launch_k1t_bf16(const __nv_bfloat16* in, __nv_bfloat16* out, int64_t tiles, float scale,
-                           cudaStream_t st) {
-  switch (k1t_bf16_variant()) {
-    case 2: return launch_k1t_x<ItemBF16M7, 12, 12, 3, SCALE>(in, out, tiles, scale, st);
-    case 3: return launch_k1t_x<ItemBF16M7, 12, 8, 2, SCALE>(in, out, tiles, scale, st);
-    case 4: return launch_k1t_x<ItemBF16M7, 12, 6, 3, SCALE>(in, out, tiles, scale, st);
-    case 5: return launch_k1t_x<ItemBF16M7, 12, 15, 3, SCALE>(in, out, tiles, scale, st);
-    default: return launch_k1t_x<ItemBF16M7, 12, 16, 2, SCALE>(in, out, tiles, scale, st);
-  }
+  return launch_k1t_x<ItemF32M12, 12, 8, 2, SCALE>(in, out, batch, scale, st);
 }
 
 // Natural-order single pass (f2): the generic K1 plan with identity store map.
@@ -283,24 +218,14 @@ chw_status dispatch_range_nat(int m, const T* in, T* out, int64_t batch, typenam
 template <class T, int M, Scaling SC>
 chw_status launch_k1(const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale,
                      cudaStream_t st) {
-  if constexpr (std::is_same<T, float>::value && M == 12) {
-    if (k1t_variant() > 0) return launch_k1t<SC == Scaling::kDeferred>(in, out, batch, scale, st);
-    if (pipeline_enabled())
-      return launch_k1p<PipeF32M12, SC == Scaling::kDeferred>(in, out, batch, scale, st);
-  }
+  if constexpr (std::is_same<T, float>::value && M == 12)
+    return launch_k1t<SC == Scaling::kDeferred>(in, out, batch, scale, st);
   using Plan = typename K1Select<T, M>::Plan;
   constexpr int TB = Plan::kTB;
   constexpr int ROWS_PER_TILE = 1 << (TB - M);
   const uint64_t full = (uint64_t)batch / ROWS_PER_TILE;
   const uint64_t tail_rows = (uint64_t)batch % ROWS_PER_TILE;
-  bool full_done = false;
-  if constexpr (std::is_same<T, __nv_bfloat16>::value && M == 7) {
-    if (full > 0 && k1t_bf16_variant() > 0) {
-      if (chw_status s = launch_k1t_bf16<SC == Scaling::kDeferred>(in, out, (int64_t)full, scale, st)) return s;
-      full_done = true;
-    }
-  }
-  if (full > 0 && !full_done) {
+  if (full > 0) {
     constexpr auto k = k1_kernel<Plan, SC, false>;
     if (chw_status s = prep_kernel<k>(Plan::SMEM_BYTES)) return s;
     for (uint64_t t0 = 0; t0 < full; t0 += 0x7fffffffull) {
@@ -349,156 +274,9 @@ chw_status launch_k4_from(const T* in, T* out, void* ws, int64_t batch,
   return CHW_OK;
 }
 
-// ---------------------------------------------------------------------------
-// K5 fused two-phase launcher (fused.cuh).
-// ---------------------------------------------------------------------------
-template <class F>
-struct FusedPlanGeom {
-  static FusedGeom make(int64_t batch) {
-    FusedGeom g{};
-    g.chunk_rows = (uint32_t)std::min<int64_t>(F::CHUNK_ROWS, batch);
-    g.nchunks = (uint32_t)((batch + g.chunk_rows - 1) / g.chunk_rows);
-    g.rows_last = (uint32_t)(batch - (int64_t)(g.nchunks - 1) * g.chunk_rows);
-    g.nA = g.chunk_rows * F::A_TILES_PER_ROW;
-    g.nB = g.chunk_rows * F::B_TILES_PER_ROW;
-    uint32_t nslots = F::NSLOTS, lag = F::LAG;
-    if (const char* e = std::getenv("CHW_B200_NSLOTS")) nslots = (uint32_t)std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("CHW_B200_LAG")) lag = (uint32_t)std::max(0, std::atoi(e));
-    g.nslots = std::min<uint32_t>(nslots, g.nchunks);
-    g.lag = std::min<uint32_t>(lag, g.nslots - 1);  // slots must outnumber the lag
-    return g;
-  }
-  static size_t slot_bytes(const FusedGeom& g) {
-    return (size_t)g.nslots * g.chunk_rows * ((size_t)1 << F::M) * sizeof(typename F::W);
-  }
-  static size_t workspace(int64_t batch) {
-    if (batch <= 0) return 0;
-    const FusedGeom g = make(batch);
-    return slot_bytes(g) + 256 + sizeof(uint32_t) * (1 + 2 * (size_t)g.nchunks);
-  }
-};
-
-template <class F, bool SCALE>
-chw_status launch_fused(const typename F::T* in, typename F::T* out, void* ws, int64_t batch,
-                        typename F::W scale, cudaStream_t st) {
-  using G = FusedPlanGeom<F>;
-  const FusedGeom g = G::make(batch);
-  if ((uint64_t)g.nchunks * (g.nA + g.nB) > 0xfffffff0ull)
-    return fail(CHW_ERR_UNSUPPORTED, "chw_forward: batch too large for the fused schedule");
-  auto* slots = static_cast<typename F::W*>(ws);
-  auto* ctr = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ((G::slot_bytes(g) + 255) & ~size_t(255)));
-  CHW_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * (1 + 2 * (size_t)g.nchunks), st));
-  if (const char* e = std::getenv("CHW_B200_FUSED"); !(e && e[0] == 'p')) {  // default: warp-specialized
-    constexpr auto kw = fused_ws_kernel<F, SCALE>;
-    constexpr int smem = FusedWS<F>::SMEM_BYTES;
-    if (chw_status s = prep_kernel<kw>(smem)) return s;
-    static int wocc[64] = {0};
-    static int wsms[64] = {0};
-    int wdev = 0;
-    if (chw_status s = current_device(&wdev)) return s;
-    if (wocc[wdev] == 0) {
-      int occ = 0, sms = 0;
-      CHW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw, F::NT + 32, smem));
-      CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wdev));
-      wocc[wdev] = std::max(1, occ);
-      wsms[wdev] = sms;
-    }
-    // All CTAs must be co-resident (items wait on items of other CTAs).
-    const uint64_t wtotal = (uint64_t)g.nchunks * (g.nA + g.nB);
-    const unsigned wgrid = (unsigned)std::min<uint64_t>(wtotal, (uint64_t)wocc[wdev] * wsms[wdev]);
-    kw<<<wgrid, F::NT + 32, smem, st>>>(in, out, slots, ctr, g, scale);
-    return check_launch("fused_ws_kernel");
-  }
-  if (pipeline_enabled()) {
-    constexpr auto kp = fused_p_kernel<F, SCALE>;
-    constexpr int smem = FusedPipe<F>::SMEM_BYTES;
-    if (chw_status s = prep_kernel<kp>(smem)) return s;
-    static int pocc[64] = {0};
-    static int psms[64] = {0};
-    int pdev = 0;
-    if (chw_status s = current_device(&pdev)) return s;
-    if (pocc[pdev] == 0) {
-      int occ = 0, sms = 0;
-      CHW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kp, F::NT, smem));
-      CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pdev));
-      pocc[pdev] = std::max(1, occ);
-      psms[pdev] = sms;
-    }
-    const uint64_t ptotal = (uint64_t)g.nchunks * (g.nA + g.nB);
-    const unsigned pgrid = (unsigned)std::min<uint64_t>(ptotal, (uint64_t)pocc[pdev] * psms[pdev]);
-    kp<<<pgrid, F::NT, smem, st>>>(in, out, slots, ctr, g, scale);
-    return check_launch("fused_p_kernel");
-  }
-  constexpr auto k = fused_kernel<F, SCALE>;
-  if (chw_status s = prep_kernel<k>(F::SMEM_BYTES)) return s;
-  static int occ_cache[64] = {0};
-  static int sms_cache[64] = {0};
-  int dev = 0;
-  if (chw_status s = current_device(&dev)) return s;
-  if (occ_cache[dev] == 0) {
-    int occ = 0, sms = 0;
-    CHW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, F::NT, F::SMEM_BYTES));
-    CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    occ_cache[dev] = std::max(1, occ);
-    sms_cache[dev] = sms;
-  }
-  const uint64_t total = (uint64_t)g.nchunks * (g.nA + g.nB);
-  const unsigned grid = (unsigned)std::min<uint64_t>(total, (uint64_t)occ_cache[dev] * sms_cache[dev]);
-  k<<<grid, F::NT, F::SMEM_BYTES, st>>>(in, out, slots, ctr, g, scale);
-  return check_launch("fused_kernel");
-}
-
-// K3 cluster launcher (cluster.cuh), f32 m = 16.
-template <bool SCALE, int XCH>
-chw_status launch_cluster_m16_x(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
-  using K = ClusterF32M16;
-  constexpr auto k = cluster_m16_kernel<SCALE, XCH>;
-  if (chw_status s = prep_kernel<k>(K::SMEM_BYTES)) return s;
-  static int ncl_cache[64] = {0};
-  int dev = 0;  // per-instantiation cache
-  if (chw_status s = current_device(&dev)) return s;
-  if (ncl_cache[dev] == 0) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(K::CLUSTER * 1024, 1, 1);
-    cfg.blockDim = dim3(K::NT, 1, 1);
-    cfg.dynamicSmemBytes = K::SMEM_BYTES;
-    int ncl = 0;
-    CHW_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
-    ncl_cache[dev] = std::max(1, ncl);
-  }
-  const uint64_t clusters = std::min<uint64_t>((uint64_t)batch, (uint64_t)ncl_cache[dev]);
-  k<<<(unsigned)(clusters * K::CLUSTER), K::NT, K::SMEM_BYTES, st>>>(in, out, (uint64_t)batch, scale);
-  return check_launch("cluster_m16_kernel");
-}
-
-template <bool SCALE>
-chw_status launch_cluster_m16(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
-  static const int xch = [] {
-    const char* e = std::getenv("CHW_B200_XCH");
-    return e ? std::atoi(e) : 1;
-  }();
-  if (xch == 0) return launch_cluster_m16_x<SCALE, 0>(in, out, batch, scale, st);
-  if (xch == 2) return launch_cluster_m16_x<SCALE, 2>(in, out, batch, scale, st);
-  return launch_cluster_m16_x<SCALE, 1>(in, out, batch, scale, st);
-}
-
-// f32 m = 16 schedule: 'c' K3 cluster/DSMEM, 'f' K5 fused dataflow, 'r<v>' K6
-// per-CTA row pipeline (rowpipe.cuh) variant v (stages x CTAs/SM, below).
-inline char m16_mode() {
-  static const char mode = [] {
-    const char* e = std::getenv("CHW_B200_M16");
-    return (e && (e[0] == 'f' || e[0] == 'r' || e[0] == 'c')) ? e[0] : 'r';
-  }();
-  return mode;
-}
-inline bool cluster_enabled() { return m16_mode() == 'c'; }
-inline int rowpipe_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("CHW_B200_M16");
-    return (e && e[0] == 'r' && e[1] >= '1' && e[1] <= '7') ? e[1] - '0' : 6;  // default: K6f (4, 6)
-  }();
-  return v;
-}
+// f32 m = 16 (cfg4): K6f, the per-CTA row pipeline (rowpipe.cuh).  The
+// measured alternatives (K3 cluster/DSMEM 47 %, K5 fused dataflow 38-41 %,
+// K6e one group per stream 55-60 %) were removed in round 2.
 
 // K6 workspace: one row per CTA (one CTA per SM).
 inline size_t rowpipe_workspace(int64_t batch) {
@@ -551,24 +329,6 @@ inline chw_status rowpipe_tmaps(void* ws, int ctas, TmapParam* t0, TmapParam* t1
 }
 
 template <bool SCALE, int SA, int SB, int HINT>
-chw_status launch_rowpipe_ws_m16_x(const float* in, float* out, void* ws, int64_t batch, float scale,
-                                   cudaStream_t st) {
-  using P = RowPipeF32M16<HINT>;
-  constexpr auto k = rowpipe_ws_kernel<P, SA, SB, SCALE>;
-  if (((uintptr_t)in | (uintptr_t)out | (uintptr_t)ws) & 15u)
-    return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers and workspace must be 16-byte aligned");
-  constexpr int smem = (SA + SB + 4) * P::TILE * 4;
-  if (chw_status s = prep_kernel<k>(smem)) return s;
-  int dev = 0, sms = 0;
-  if (chw_status s = current_device(&dev)) return s;
-  CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = (int)std::min<int64_t>(batch, (int64_t)sms);
-  TmapParam t0, t1;
-  if (chw_status s = rowpipe_tmaps(ws, grid, &t0, &t1)) return s;
-  k<<<grid, 2 * P::NT + 64, smem, st>>>(in, out, static_cast<float*>(ws), (uint64_t)batch, scale, t0, t1);
-  return check_launch("rowpipe_ws_kernel");
-}
-template <bool SCALE, int SA, int SB, int HINT>
 chw_status launch_rowpipe_ws4_m16_x(const float* in, float* out, void* ws, int64_t batch, float scale,
                                     cudaStream_t st) {
   using P = RowPipeF32M16<HINT>;
@@ -590,28 +350,16 @@ chw_status launch_rowpipe_ws4_m16_x(const float* in, float* out, void* ws, int64
   return check_launch("rowpipe_ws4_kernel");
 }
 
-// Variants (measured): K6e (one compute group per stream)
-// r1..r4 with ring depths (A, B) and L2 hints; K6f (two groups per stream,
-// even ring depths) r5..r7.  Default r6.
+// K6f default: rings of 4 A stages and 6 B stages, two compute groups per
+// stream, evict-first input / evict-last workspace hints.
 template <bool SCALE>
 chw_status launch_rowpipe_m16(const float* in, float* out, void* ws, int64_t batch, float scale,
                               cudaStream_t st) {
-  switch (rowpipe_variant()) {
-    case 2: return launch_rowpipe_ws_m16_x<SCALE, 6, 4, 3>(in, out, ws, batch, scale, st);
-    case 3: return launch_rowpipe_ws_m16_x<SCALE, 5, 5, 1>(in, out, ws, batch, scale, st);
-    case 4: return launch_rowpipe_ws_m16_x<SCALE, 7, 3, 1>(in, out, ws, batch, scale, st);
-    case 5: return launch_rowpipe_ws4_m16_x<SCALE, 6, 4, 1>(in, out, ws, batch, scale, st);
-    case 6: return launch_rowpipe_ws4_m16_x<SCALE, 4, 6, 1>(in, out, ws, batch, scale, st);
-    case 7: return launch_rowpipe_ws4_m16_x<SCALE, 8, 2, 1>(in, out, ws, batch, scale, st);
-    default: return launch_rowpipe_ws_m16_x<SCALE, 6, 4, 1>(in, out, ws, batch, scale, st);
-  }
+  return launch_rowpipe_ws4_m16_x<SCALE, 4, 6, 1>(in, out, ws, batch, scale, st);
 }
 
-// Two-pass static pipelined schedule for f32 m = 24 (BASELINE cfg5): rows in
-// chunks of kM24Chunk; per chunk pass A (input -> intermediate) then pass B
-// (intermediate -> dyadic output), each a statically scheduled pipelined
-// kernel.  Measured: 38.5 % of HBM peak vs 31 % for the
-// one-launch dataflow schedule, whose dependency waits drain the pipelines.
+// m = 24 (cfg5).  K4T: two statically scheduled passes through an HBM
+// intermediate in 16-row chunks (both passes TMA-fed).
 constexpr int64_t kM24Chunk = 16;  // rows per chunk: 1 GiB intermediate
 // K4T rows per chunk (CHW_B200_M24_CHUNK=1..16; default 16).
 inline int64_t m24_chunk_rows() {
@@ -622,41 +370,23 @@ inline int64_t m24_chunk_rows() {
   }();
   return v;
 }
-template <bool SCALE>
-chw_status launch_two_pass_m24(const float* in, float* out, void* ws, int64_t batch, float scale,
-                               cudaStream_t st) {
-  using P = FusedPipe<FusedF32M24>;
-  constexpr int S = 2, NT = FusedF32M24::NT, MINB = 1;
-  constexpr int smem = (S + 1) * P::TILE * 4;
-  constexpr auto ka = pass_p_kernel<P::ItemA, GeoA24, false, S, NT, MINB>;
-  constexpr auto kb = pass_p_kernel<P::ItemB, GeoB24, SCALE, S, NT, MINB>;
-  if (chw_status s = prep_kernel<ka>(smem)) return s;
-  if (chw_status s = prep_kernel<kb>(smem)) return s;
-  const int64_t chunk = kM24Chunk;
-  int dev = 0, sms = 0;
-  if (chw_status s = current_device(&dev)) return s;
-  CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  float* mid = static_cast<float*>(ws);
-  for (int64_t r0 = 0; r0 < batch; r0 += chunk) {
-    const int64_t rows = std::min<int64_t>(chunk, batch - r0);
-    const uint64_t items = (uint64_t)rows * 1024;
-    const unsigned grid = (unsigned)std::min<uint64_t>(items, (uint64_t)sms * MINB);
-    ka<<<grid, NT, smem, st>>>(in + ((uint64_t)r0 << 24), mid, items, scale);
-    if (chw_status s = check_launch("pass_p_kernel(A)")) return s;
-    kb<<<grid, NT, smem, st>>>(mid, out + ((uint64_t)r0 << 24), items, scale);
-    if (chw_status s = check_launch("pass_p_kernel(B)")) return s;
-  }
-  return CHW_OK;
-}
-
-// f32 m = 24 schedule: 't' K4T (default), 'p' K4P, 'f' K5 fused dataflow.
+// f32 m = 24 schedule: 's' K9 row sweep (default), 't' K4T two-pass.  (K4P
+// and the K5 dataflow kernels were measured slower and removed in round 2.)
 inline char m24_mode() {
   static const char mode = [] {
     const char* e = std::getenv("CHW_B200_M24");
-    return (e && (e[0] == 't' || e[0] == 'p' || e[0] == 'f')) ? e[0] : 't';
+    return (e && e[0] == 't') ? 't' : 's';
   }();
   return mode;
 }
+// K9 workspace: one row (64 MiB, L2-resident) + one completion counter per row.
+inline size_t sweep_m24_workspace(int64_t batch) {
+  return ((size_t)64 << 20) + (((size_t)std::max<int64_t>(batch, 0) * 4 + 255) & ~(size_t)255);
+}
+// K9 launcher (sweep.cu, its own translation unit).
+chw_status launch_sweep_m24(bool scale_mode, const float* in, float* out, void* ws, int64_t batch, float scale,
+                            cudaStream_t st);
+
 // K4T (passtma.cuh): the K4P two-pass schedule fed by TMA, in-place tile
 // transposes (3 tiles in flight per SM).  Same-box A/B: 42.8-42.9 % vs K4P
 // 37.9-38.0 % of HBM peak (profiles/r01_ab_k4t.txt).
@@ -710,19 +440,6 @@ chw_status launch_two_pass_tma_m24(const float* in, float* out, void* ws, int64_
   return CHW_OK;
 }
 
-// Fused spec per (T, M), void when none exists (the K4 multi-pass path is used).
-template <class T, int M>
-struct FusedSelect {
-  using F = void;
-};
-template <>
-struct FusedSelect<float, 16> {
-  using F = FusedF32M16b;
-};
-template <>
-struct FusedSelect<float, 24> {
-  using F = FusedF32M24;
-};
 
 template <class T, int MLO = Regime<T>::K1MAX + 1>
 size_t k4_workspace_m(int m, int64_t batch, size_t inter) {
@@ -730,16 +447,13 @@ size_t k4_workspace_m(int m, int64_t batch, size_t inter) {
     return 0;
   } else {
     if (m != MLO) return k4_workspace_m<T, MLO + 1>(m, batch, inter);
-    using F = typename FusedSelect<T, MLO>::F;
-    if constexpr (!std::is_void<F>::value) {
-      size_t w = FusedPlanGeom<F>::workspace(batch);
-      if constexpr (std::is_same<T, float>::value && MLO == 16) w = std::max(w, rowpipe_workspace(batch));
-      if constexpr (std::is_same<T, float>::value && MLO == 24)
-        w = std::max(w, (size_t)std::min<int64_t>(batch, kM24Chunk) << 26);  // two-pass intermediate
-      return w;
-    } else {
-      return (size_t)batch * ((size_t)1 << m) * inter;
+    if (batch <= 0) return 0;
+    if constexpr (std::is_same<T, float>::value && MLO == 16) return rowpipe_workspace(batch);
+    if constexpr (std::is_same<T, float>::value && MLO == 24) {
+      if (m24_mode() == 's') return sweep_m24_workspace(batch);  // K9: one L2-resident row
+      return (size_t)std::min<int64_t>(batch, kM24Chunk) << 26;  // K4T: 16-row intermediate
     }
+    return (size_t)batch * ((size_t)1 << m) * inter;
   }
 }
 
@@ -748,18 +462,11 @@ chw_status launch_m(const T* in, T* out, void* ws, int64_t batch, typename IoTra
                     cudaStream_t st) {
   if constexpr (M <= Regime<T>::K1MAX) {
     return launch_k1<T, M, SC>(in, out, batch, scale, st);
-  } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {
-    if constexpr (std::is_same<T, float>::value && M == 16) {
-      if (cluster_enabled()) return launch_cluster_m16<SC == Scaling::kDeferred>(in, out, batch, scale, st);
-      if (m16_mode() == 'r') return launch_rowpipe_m16<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
-    }
-    if constexpr (std::is_same<T, float>::value && M == 24) {
-      const char m24 = m24_mode();
-      if (m24 == 't') return launch_two_pass_tma_m24<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
-      if (m24 == 'p') return launch_two_pass_m24<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
-    }
-    return launch_fused<typename FusedSelect<T, M>::F, SC == Scaling::kDeferred>(in, out, ws, batch,
-                                                                                 scale, st);
+  } else if constexpr (std::is_same<T, float>::value && M == 16) {
+    return launch_rowpipe_m16<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
+  } else if constexpr (std::is_same<T, float>::value && M == 24) {
+    if (m24_mode() == 's') return launch_sweep_m24(SC == Scaling::kDeferred, in, out, ws, batch, scale, st);
+    return launch_two_pass_tma_m24<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
   } else {
     return launch_k4_from<T, M, SC, 0>(in, out, ws, batch, scale, st);
   }
@@ -783,17 +490,12 @@ const char* plan_name_m(int m) {
   } else {
     if (m != M) return plan_name_m<T, M + 1>(m);
     if constexpr (M <= Regime<T>::K1MAX) {
-      if constexpr (std::is_same<T, float>::value && M == 12)
-        if (k1t_variant() > 0) return "k1t-tma";
-      if constexpr (std::is_same<T, __nv_bfloat16>::value && M == 7)
-        if (k1t_bf16_variant() > 0) return "k1t-tma";
+      if constexpr (std::is_same<T, float>::value && M == 12) return "k1t-tma";
       return K1Select<T, M>::kTuned ? "k1-tuned" : "k1-generic";
     } else if constexpr (std::is_same<T, float>::value && M == 16) {
-      return m16_mode() == 'c' ? "k3-cluster-dsmem" : m16_mode() == 'r' ? "k6-rowpipe" : "k5-fused-2phase";
+      return "k6-rowpipe";
     } else if constexpr (std::is_same<T, float>::value && M == 24) {
-      return m24_mode() == 't' ? "k4t-two-pass-tma" : m24_mode() == 'p' ? "k4p-two-pass-pipelined" : "k5-fused-2phase";
-    } else if constexpr (!std::is_void<typename FusedSelect<T, M>::F>::value) {
-      return "k5-fused-2phase";
+      return m24_mode() == 's' ? "k9-row-sweep" : "k4t-two-pass-tma";
     } else {
       static const std::string s = "k4-multipass:" + std::to_string(K4Sched<T, M>::NPASS);
       return s.c_str();

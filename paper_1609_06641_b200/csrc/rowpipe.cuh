@@ -130,130 +130,6 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t count) {
 }
 
 // ---------------------------------------------------------------------------
-// K6e: warp-specialized row pipeline.  One CTA per SM, one workspace row per
-// CTA (37 MiB).  Roles:
-//   warp 8 lane 0  : A producer — bulk copies of input tiles into ring A;
-//   warp 9 lane 0  : B producer — tensor copies of workspace tiles into ring B,
-//                    row i only after A(i,15) is stored (rowstored barrier);
-//   warps 0-3 (gA) : A stream A(0,0..15), A(1,0..15), ... -> workspace;
-//   warps 4-7 (gB) : B stream -> dyadic output.
-// The two compute groups never share a CTA barrier; they meet only where the
-// data does: A(i,k) stores wait for B(i-1,k) to have consumed region k
-// (regionfree[k]), B(i,.) loads wait for A(i,15) (rowstored).  Each group
-// double-buffers its transpose tile, so one named barrier per item suffices.
-// ---------------------------------------------------------------------------
-template <class P, int SA, int SB, bool SCALE>
-__global__ void __launch_bounds__(2 * P::NT + 64, 1)
-    rowpipe_ws_kernel(const float* __restrict__ in, float* __restrict__ out, float* __restrict__ ws, uint64_t rows,
-                      float scale, const __grid_constant__ TmapParam tmap0, const __grid_constant__ TmapParam tmap1) {
-  constexpr int TILE = P::TILE;
-  constexpr uint32_t TB = TILE * 4;
-  constexpr uint64_t n = 1ull << P::M;
-  constexpr int NT = P::NT;
-  extern __shared__ __align__(128) float smem_ws[];
-  float* ringA = smem_ws;
-  float* ringB = smem_ws + SA * TILE;
-  float* workA = smem_ws + (SA + SB) * TILE;  // 2 tiles
-  float* workB = workA + 2 * TILE;            // 2 tiles
-  __shared__ __align__(8) uint64_t fullA[SA], emptyA[SA], fullB[SB], emptyB[SB], regionfree[16], rowstored;
-  const uint32_t tid = threadIdx.x;
-  const uint64_t G = gridDim.x;
-  const uint64_t c = blockIdx.x;
-  if (c >= rows) return;
-  const uint32_t R = (uint32_t)((rows - 1 - c) / G + 1);
-  const uint32_t nst = 16u * R;  // items per stream
-  float* wsc = ws + c * n;
-  if (tid == 0) {
-    for (int s = 0; s < SA; ++s) {
-      mbar_init_cta(&fullA[s], 1);
-      mbar_init_cta(&emptyA[s], 1);
-    }
-    for (int s = 0; s < SB; ++s) {
-      mbar_init_cta(&fullB[s], 1);
-      mbar_init_cta(&emptyB[s], 1);
-    }
-    for (int k = 0; k < 16; ++k) mbar_init_cta(&regionfree[k], 1);
-    mbar_init_cta(&rowstored, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const uint32_t warp = tid >> 5, lane = tid & 31u;
-  if (warp >= 8) {
-    if (lane != 0) return;
-    if (warp == 8) {  // A producer
-      const uint64_t pol_in = (P::HINT & 1) ? l2_evict_first_policy() : l2_evict_normal_policy();
-      for (uint32_t t = 0; t < nst; ++t) {
-        const int st = t % SA;
-        if (t >= (uint32_t)SA) mbar_wait_cta(&emptyA[st], ((t / SA) - 1) & 1u);
-        mbar_expect_tx_cta(&fullA[st], TB);
-        bulk_g2s(ringA + st * TILE, in + (c + (uint64_t)(t >> 4) * G) * n + ((t & 15u) << 12), TB, &fullA[st],
-                 pol_in);
-      }
-    } else {  // B producer
-      for (uint32_t t = 0; t < nst; ++t) {
-        const uint32_t i = t >> 4, kk = t & 15u;
-        if (kk == 0) mbar_wait_cta(&rowstored, i & 1u);
-        const int st = t % SB;
-        if (t >= (uint32_t)SB) mbar_wait_cta(&emptyB[st], ((t / SB) - 1) & 1u);
-        mbar_expect_tx_cta(&fullB[st], TB);
-        if (i & 1u)
-          tensor4_g2s(ringB + st * TILE, &tmap1, 0, 0, 0, (int)(c * 16u + kk), &fullB[st]);
-        else
-          tensor3_g2s(ringB + st * TILE, &tmap0, 0, (int)kk, (int)(c * 256u), &fullB[st]);
-      }
-    }
-    return;
-  }
-  const uint32_t grp = warp >> 2;  // 0: A stream, 1: B stream
-  const uint32_t gt = tid & (NT - 1);
-  float v[P::ItemA0::E];
-  if (grp == 0) {
-    for (uint32_t t = 0; t < nst; ++t) {
-      const int st = t % SA;
-      const uint32_t i = t >> 4, kk = t & 15u;
-      float* work = workA + (t & 1u) * TILE;
-      mbar_wait_cta(&fullA[st], (t / SA) & 1u);
-      P::ItemA0::phase0(ringA + st * TILE, work, v, gt);
-      named_bar(1, NT);
-      if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&emptyA[st])) : "memory");
-      if (i >= 1) mbar_wait_cta(&regionfree[kk], (i - 1) & 1u);  // B(i-1,kk) consumed region kk
-      float* dst = wsc + P::a_off(kk, i & 1u);
-      if constexpr (P::HINT_DISCARD) {
-        if (!(i & 1u)) {
-          discard_l2_128(dst + gt * 32u);
-          named_bar(1, NT);  // every line dropped before any thread stores into it
-        }
-      }
-      if (i & 1u)
-        P::ItemA1::template phase1<false>(work, dst, v, gt, scale);
-      else
-        P::ItemA0::template phase1<false>(work, dst, v, gt, scale);
-      if (kk == 15u) {
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        named_bar(1, NT);
-        if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&rowstored)) : "memory");
-      }
-    }
-  } else {
-    for (uint32_t t = 0; t < nst; ++t) {
-      const int st = t % SB;
-      const uint32_t i = t >> 4, kk = t & 15u;
-      float* work = workB + (t & 1u) * TILE;
-      mbar_wait_cta(&fullB[st], (t / SB) & 1u);
-      P::ItemB0::phase0(ringB + st * TILE, work, v, gt);
-      named_bar(2, NT);
-      if (gt == 0) {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&emptyB[st])) : "memory");
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[kk])) : "memory");
-      }
-      const uint64_t row = c + (uint64_t)i * G;
-      P::ItemB0::template phase1<SCALE>(work, out + row * n + deposit<P::F::B::OuterOut>(kk), v, gt, scale);
-    }
-  }
-}
-
-
-// ---------------------------------------------------------------------------
 // K6f: K6e with two compute groups per stream (16 compute warps per SM).
 // Group (s, p) runs the items t = p (mod 2) of stream s; transpose tiles are
 // single-buffered (two named barriers per item).  rowstored counts both A

@@ -99,7 +99,7 @@ def test_plan_selection():
     assert chw.plan_name(chw.DTYPE_F32, 4096) == "k1t-tma"
     assert chw.plan_name(chw.DTYPE_BF16, 128) == "k1-tuned"
     assert chw.plan_name(chw.DTYPE_F64, 1024).startswith("k1")
-    assert chw.plan_name(chw.DTYPE_F32, 1 << 24) == "k4t-two-pass-tma"
+    assert chw.plan_name(chw.DTYPE_F32, 1 << 24) == "k9-row-sweep"
     assert chw.plan_name(chw.DTYPE_F32, 1 << 16) == "k6-rowpipe"
     assert chw.plan_name(chw.DTYPE_F32, 1 << 20).startswith("k4-multipass")
 

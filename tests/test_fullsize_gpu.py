@@ -124,3 +124,25 @@ def test_fullsize_exact_order_probe(cuda, cfg):
         got = x.index_select(0, it).to(torch.float64).cpu().numpy()
         want = oracle.chw_batch(xs, oracle.UNNORMALIZED, backend=BACKEND, threads=0)
         assert np.array_equal(got, want.astype(np.float64)), f"{cfg}: order probe mismatch in rows {sub[0]}.."
+
+
+def test_cfg5_fresh_process_all_rows_device_equals_host_path(cuda):
+    """Race detector for the single-pass m = 24 sweep: in a FRESH process (cold
+    caches, first launch), the full cfg5 batch through the device path must
+    equal, bit for bit and on every one of the 256 rows, repeated device runs
+    and the host-buffer path (one-row chunks on two streams: different timing);
+    a few rows are also checked against the C port.  (A missing async-proxy
+    fence once corrupted one thread's 128 outputs of one row on the first run
+    only — the kind of bug sampled-row parity cannot see.)"""
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(repo, "tools", "stress_m24.py"), "256", "2"],
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+    assert "differ" not in p.stdout, p.stdout
+    for line in p.stdout.splitlines():
+        if line.startswith("oracle row"):
+            assert float(line.split()[-1]) <= 1e-5, line
