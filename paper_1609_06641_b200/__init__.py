@@ -30,7 +30,8 @@ from dataclasses import dataclass, field
 from typing import List, Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libchw_b200.so")
+# CHW_B200_LIB overrides the library path (same-box A/B of alternative builds).
+LIB_PATH = os.environ.get("CHW_B200_LIB") or os.path.join(_HERE, "libchw_b200.so")
 
 # C-ABI enums (include/chw_b200.h)
 CHW_OK = 0

@@ -499,6 +499,16 @@ __device__ __forceinline__ void bf2(float& a0, float& a1, float& b0, float& b1) 
   asm("mov.b64 {%0, %1}, %2;" : "=f"(b0), "=f"(b1) : "l"(D));
 }
 
+// Two fp32 products a*s, b*s in one packed FMUL2 (sm_100 mul.rn.f32x2),
+// each rounded exactly like __fmul_rn.
+__device__ __forceinline__ void mul2(float& a, float& b, float s) {
+  uint64_t A, S, P;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(a), "f"(b));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(S) : "f"(s));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(P) : "l"(A), "l"(S));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(P));
+}
+
 // Butterflies on the listed tile bits, in list order (order matters only for
 // bit-exact f64; f32/bf16 are order-free up to rounding).  fp32 butterflies on
 // register bits other than bit 0 are issued in pairs (registers r, r^1) as
@@ -515,6 +525,9 @@ __device__ __forceinline__ void butterflies(C (&v)[L::E]) {
           if constexpr (!((r >> k) & 1)) bf2(v[r], v[r | 1], v[r | (1 << k)], v[(r | (1 << k)) | 1]);
         });
       } else {
+        // register bit 0 stays scalar: pairing (r, r|2) for it would fight the
+        // (r, r|1) register pairs of every other bit (measured: the repacking
+        // MOVs cost more than the saved FADDs, cfg5 0.53 -> 0.49).
         static_for<L::E>([&](auto R) {
           constexpr int r = decltype(R)::value;
           if constexpr (!((r >> k) & 1)) bf<PER_STAGE>(v[r], v[r | (1 << k)]);
@@ -607,9 +620,15 @@ __device__ __forceinline__ void store_global(T* __restrict__ base, const C (&v)[
       C tmp[1 << VB];
       static_for<(1 << VB)>([&](auto Q) {
         constexpr int q = decltype(Q)::value;
-        const C x = v[vec_elem<L, Map>(r, q, VB)];
-        tmp[q] = SCALE ? x * scale : x;
+        tmp[q] = v[vec_elem<L, Map>(r, q, VB)];
       });
+      if constexpr (SCALE) {
+        if constexpr (std::is_same<C, float>::value && VB >= 1) {
+          static_for<(1 << VB) / 2>([&](auto Q) { mul2(tmp[2 * decltype(Q)::value], tmp[2 * decltype(Q)::value + 1], scale); });
+        } else {
+          static_for<(1 << VB)>([&](auto Q) { tmp[decltype(Q)::value] *= scale; });
+        }
+      }
       VecIO<T, VB, CO>::st(base + (tb + ro), tmp);
     }
   });

@@ -36,6 +36,15 @@
 
 #include "passtma.cuh"
 
+#ifndef CHW_SWEEP_OPAQUE
+#define CHW_SWEEP_OPAQUE 1
+#endif
+// Debug builds (-DCHW_SWEEP_TRACE=1, tools/sweep_trace.py) record %globaltimer
+// stamps per tile for CTAs 0 and 1: [cta][group][item][event].
+#ifndef CHW_SWEEP_TRACE
+#define CHW_SWEEP_TRACE 0
+#endif
+
 namespace chwb {
 
 struct SweepF32M24 {
@@ -66,7 +75,8 @@ struct SweepF32M24 {
   using BH1 = Layout<BL<12, 11, 3, 4, 5, 0>, BL<10, 9, 8, 7, 6, 1, 2>>;
   using BHS = Swz<7, 1, 8, 2, 9, 3, 10, 4>;
   static constexpr int BL0_T0 = 0;  // register bit of t0 in BL0
-  static constexpr int BL1_T0 = 5;  // register bit of t0 in BL1
+  using BHB1 = BL<3, 4, 5, 11, 12>;                                      // BB1 in half numbering
+  using BOutH = ListMap<20, 18, 17, 9, 8, 7, 6, 5, 4, 3, 2, 1, 0>;       // BOut without t0 (out bit 21)
   // dyadic output position (bit q = j bit 23 - q) of tile bit t, and of the
   // B tile index bits (v0..v9 = j0,j1,j7,j8,j9,j4,j10,j11,j12,j13).
   using BOut = ListMap<21, 20, 18, 17, 9, 8, 7, 6, 5, 4, 3, 2, 1, 0>;
@@ -129,24 +139,6 @@ __device__ __forceinline__ void smem_load_half(const float* sm, float (&w)[E2], 
     }
   });
 }
-template <class Lh, class S, int SLOT, int HV, int E>
-__device__ __forceinline__ void smem_load_half_into(const float* sm, float (&v)[E], uint32_t tid) {
-  constexpr int VB = smem_vec_bits<Lh, S, 2>();
-  constexpr uint32_t tmask = S::image(thr_mask<Lh, IdMap>());
-  const uint32_t sb = S::apply(thr_off<Lh, IdMap>(tid));
-  static_for<Lh::E>([&](auto R) {
-    constexpr int rh = decltype(R)::value;
-    if constexpr (vec_head<Lh, IdMap>(rh, VB)) {
-      constexpr uint32_t so = S::apply(reg_off<Lh, IdMap>(rh));
-      const uint32_t a = (so & tmask) ? (sb ^ so) : (sb + so);
-      float tmp[1 << VB];
-      SmemVec<float, VB>::ld(sm + a, tmp);
-      static_for<(1 << VB)>([&](auto Q) {
-        v[ins_bit(vec_elem<Lh, IdMap>(rh, decltype(Q)::value, VB), SLOT, HV)] = tmp[decltype(Q)::value];
-      });
-    }
-  });
-}
 __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -162,6 +154,23 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
 // are counted (acquire + async-proxy fence); B(r, i)'s bytes landing in
 // shared memory free its workspace region, so the B group signals
 // `regionfree[i]` as soon as the stage is full and A(r+1, i) may overwrite it.
+#if CHW_SWEEP_TRACE
+__device__ unsigned long long* g_sweep_trace = nullptr;
+__device__ __forceinline__ void trace_stamp(uint32_t cta, uint32_t grp, uint32_t item, uint32_t ev) {
+  if (g_sweep_trace && cta < 2 && item < 512) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_sweep_trace[((cta * 2 + grp) * 512 + item) * 8 + ev] = t;
+  }
+}
+#define SWEEP_STAMP(grp, ev) \
+  if (gt == 0) trace_stamp(c, grp, u, ev)
+#else
+#define SWEEP_STAMP(grp, ev) \
+  do {                       \
+  } while (0)
+#endif
+
 template <bool SCALE>
 __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
     sweep_m24_kernel(const float* __restrict__ in, float* __restrict__ out, float* __restrict__ ws,
@@ -205,17 +214,25 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       pol = l2_evict_first_policy();
       for (uint32_t u = 0; u < (uint32_t)SA && u < total; ++u) issue(u);
     }
-    for (uint32_t u = 0; u < total; ++u) {
-      const uint32_t r = u / nt, i = u - r * nt;
+    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
       const int st = (int)(u % SA);
       float* stage = ringA + st * TILE;
+      // Opaque copy of the thread index: keeps the per-register swizzled
+      // shared-memory addresses inside the loop (hoisted, they need ~20 live
+      // registers and spill).
+      uint32_t gtv = gt;
+#if CHW_SWEEP_OPAQUE
+      asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
+#endif
+      SWEEP_STAMP(0, 0);
       mbar_wait_cta(&fullA[st], (u / SA) & 1u);
-      smem_load<P::AL0, NoSwz>(stage, v, gt);
+      SWEEP_STAMP(0, 1);
+      smem_load<P::AL0, NoSwz>(stage, v, gtv);
       butterflies<P::AL0, P::AB0, false>(v);
       bar();
-      smem_store<P::AL0, P::AS>(stage, v, gt);
+      smem_store<P::AL0, P::AS>(stage, v, gtv);
       bar();
-      smem_load<P::AL1, P::AS>(stage, v, gt);
+      smem_load<P::AL1, P::AS>(stage, v, gtv);
       bar();  // every thread has read the stage: refill it
       if (gt == 0 && u + SA < total) {
         // order the group's generic-proxy reads of the stage before the TMA write
@@ -223,17 +240,20 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
         issue(u + SA);
       }
       butterflies<P::AL1, P::AB1, false>(v);
+      SWEEP_STAMP(0, 2);
       if (r >= 1) mbar_wait_cta(&regionfree[i], (r - 1) & 1u);  // B(r-1, a) has been read
+      SWEEP_STAMP(0, 3);
       const uint32_t a = c + i * G;
       if (r & 1u)
-        store_global<P::AL1, P::AOutQ, false, Cache::kL2>(ws + ((uint64_t)a << 4), v, gt, 1.0f);
+        store_global<P::AL1, P::AOutQ, false, Cache::kL2>(ws + ((uint64_t)a << 4), v, gtv, 1.0f);
       else
-        store_global<P::AL1, P::AOutP, false, Cache::kL2>(ws + ((uint64_t)a << 14), v, gt, 1.0f);
+        store_global<P::AL1, P::AOutP, false, Cache::kL2>(ws + ((uint64_t)a << 14), v, gtv, 1.0f);
       if (i + 1 == nt) {  // this CTA's last A tile of row r: publish all nt of them
         asm volatile("fence.proxy.async.global;" ::: "memory");  // other CTAs read them with TMA
         bar();
         if (gt == 0) red_release_add(&cnt[r], nt);
       }
+      SWEEP_STAMP(0, 4);
     }
   } else {  // ---- B group
     const uint32_t gt = tid - NT;
@@ -265,13 +285,19 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       pol = l2_evict_normal_policy();
       pending = total > 0;
     }
-    for (uint32_t u = 0; u < total; ++u) {
-      const uint32_t r = u / nt, i = u - r * nt;
+    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
+      SWEEP_STAMP(1, 0);
       if (pending) pending = !issue(u, true);
+      SWEEP_STAMP(1, 1);
+      uint32_t gtv = gt;  // opaque thread index (see the A loop)
+#if CHW_SWEEP_OPAQUE
+      asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
+#endif
       mbar_wait_cta(&fullB, u & 1u);
+      SWEEP_STAMP(1, 2);
       // B(r, t)'s workspace bytes are in shared memory: A(r+1, t) may overwrite them.
       if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
-      smem_load<P::BL0, NoSwz>(stageB, v, gt);
+      smem_load<P::BL0, NoSwz>(stageB, v, gtv);
       bar();  // the stage is read: load the next B tile while this one is computed
       if (gt == 0 && u + 1 < total) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -279,22 +305,213 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       }
       butterflies<P::BL0, P::BB0, false>(v);
       // L0 -> L1 through the 32 KiB buffer, t0 = 0 half then t0 = 1 half.
-      float w[P::E / 2];
-      smem_store_half<P::BH0, P::BHS, P::BL0_T0, 0>(bufB, v, gt);
-      bar();
-      smem_load_half<P::BH1, P::BHS>(bufB, w, gt);
-      bar();
-      smem_store_half<P::BH0, P::BHS, P::BL0_T0, 1>(bufB, v, gt);
-      bar();
-      smem_load_half_into<P::BH1, P::BHS, P::BL1_T0, 1>(bufB, v, gt);  // v's L0 values are all stored
-      static_for<P::E / 2>([&](auto R) {
-        constexpr int rh = decltype(R)::value;
-        v[ins_bit(rh, P::BL1_T0, 0)] = w[rh];
-      });
-      butterflies<P::BL1, P::BB1, false>(v);
+      // L0 -> L1 through the 32 KiB buffer one t0-half at a time; B1 (which
+      // never touches t0) and the stores run per half, so only 64 extra
+      // registers are live.
       const uint32_t t = c + i * G;
-      store_global<P::BL1, P::BOut, SCALE, Cache::kStream>(out + ((uint64_t)r << 24) + deposit<P::BOuter>(t), v,
-                                                            gt, scale);
+      float* orow = out + ((uint64_t)r << 24) + deposit<P::BOuter>(t);
+      float w[P::E / 2];
+      smem_store_half<P::BH0, P::BHS, P::BL0_T0, 0>(bufB, v, gtv);
+      bar();
+      smem_load_half<P::BH1, P::BHS>(bufB, w, gtv);
+      bar();
+      smem_store_half<P::BH0, P::BHS, P::BL0_T0, 1>(bufB, v, gtv);
+      butterflies<P::BH1, P::BHB1, false>(w);
+      store_global<P::BH1, P::BOutH, SCALE, Cache::kStream>(orow, w, gtv, scale);
+      bar();
+      smem_load_half<P::BH1, P::BHS>(bufB, w, gtv);
+      butterflies<P::BH1, P::BHB1, false>(w);
+      store_global<P::BH1, P::BOutH, SCALE, Cache::kStream>(orow + (1u << 21), w, gtv, scale);
+      SWEEP_STAMP(1, 3);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K9b: the same single-pass sweep with 64-value threads and 16 warps per SM
+// (4 per sub-partition instead of 2: the 128-value version was latency bound,
+// IPC ~0.15 per warp, tools/sweep_trace.py).  A tiles (64 KiB, 256 threads)
+// take three layouts (j0, j1 stay in registers throughout, so every shared
+// round trip is a 16-byte vector access); B tiles shrink to 32 KiB (3
+// passengers = 32-byte runs + j14..23, 128 threads, three layouts), two per
+// A tile, handled by two B groups with one 32 KiB stage each.
+//
+// Workspace (layout P, even rows): addr[0..2] = passengers (j0, j1, j5),
+// addr[3..13] = v (B tile index, 11 bits), addr[14..23] = a (j14..23).
+// Layout Q (odd rows): addr[0..2] passengers, addr[3..12] = a,
+// addr[13..23] = v.  A(r+1, a) overwrites exactly B(r, a), B(r, a + 1024)
+// (r even) or B(r, 2a), B(r, 2a + 1) (r odd): CTA c owns A tiles
+// a_i = c + i G and those B tiles; B group g takes the g-th of each pair.
+// ---------------------------------------------------------------------------
+struct SweepBF32M24 {
+  static constexpr int M = 24;
+  static constexpr int ATILE = 1 << 14, BTILE = 1 << 13;
+  static constexpr int NTA = 256, NTB = 128;
+  static constexpr uint32_t NTILES = 1024;  // A tiles per row (B tiles: 2048)
+  // A: tile bit k = j bit k.
+  using AL0 = Layout<BL<0, 1, 5, 6, 7, 8>, BL<2, 3, 4, 9, 10, 11, 12, 13>>;
+  using AL1 = Layout<BL<0, 1, 2, 3, 4, 9>, BL<5, 6, 7, 8, 10, 11, 12, 13>>;
+  using AL2 = Layout<BL<0, 1, 10, 11, 12, 13>, BL<5, 6, 7, 8, 9, 2, 3, 4>>;
+  using AS1 = Swz<5, 2, 6, 3, 7, 4>;
+  using AS2 = Swz<5, 2, 6, 3, 7, 4>;
+  using AB0 = BL<0, 1, 5, 6, 7, 8>;
+  using AB1 = BL<2, 3, 4, 9>;
+  using AB2 = BL<10, 11, 12, 13>;
+  // passengers j0, j1, j5 -> addr 0..2; v0..v10 = j6, j7, j8, j9, j2, j3, j4, j10..j13
+  using AOutP = ListMap<0, 1, 7, 8, 9, 2, 3, 4, 5, 6, 10, 11, 12, 13>;         // tile base a << 14
+  using AOutQ = ListMap<0, 1, 17, 18, 19, 2, 13, 14, 15, 16, 20, 21, 22, 23>;  // tile base a << 3
+  // B: t0..t2 = passengers (addr 0..2), t3..t12 = j14..j23.
+  using BL0 = Layout<BL<0, 1, 7, 8, 9, 10>, BL<2, 3, 4, 5, 6, 11, 12>>;
+  using BL1 = Layout<BL<0, 1, 3, 4, 5, 6>, BL<7, 8, 9, 10, 2, 11, 12>>;
+  using BL2 = Layout<BL<12, 11, 0, 1, 3, 4>, BL<10, 9, 8, 7, 2, 5, 6>>;
+  using BS1 = Swz<7, 2, 8, 3, 9, 4>;
+  using BS2 = Swz<7, 2, 10, 2, 8, 3, 9, 4>;
+  using BB0 = BL<7, 8, 9, 10>;
+  using BB1 = BL<3, 4, 5, 6>;
+  using BB2 = BL<11, 12>;
+  // dyadic output position (bit q = j bit 23 - q) of tile bit t and of v's bits
+  using BOut = ListMap<23, 22, 18, 9, 8, 7, 6, 5, 4, 3, 2, 1, 0>;
+  using BOuter = BL<17, 16, 15, 14, 21, 20, 19, 13, 12, 11, 10>;
+  static_assert(AL0::NT == NTA && BL0::NT == NTB && AL0::E == 64 && BL0::E == 64, "group shape");
+};
+
+template <bool SCALE>
+__global__ void __launch_bounds__(SweepBF32M24::NTA + 2 * SweepBF32M24::NTB, 1)
+    sweep_b_m24_kernel(const float* __restrict__ in, float* __restrict__ out, float* __restrict__ ws,
+                       uint32_t* __restrict__ cnt, uint32_t rows, float scale,
+                       const __grid_constant__ TmapParam tmapP) {
+  using P = SweepBF32M24;
+  constexpr uint32_t TBA = P::ATILE * 4, TBB = P::BTILE * 4;
+  constexpr int SA = 2;
+  constexpr int MAXT = 8;
+  extern __shared__ __align__(128) float smem_sb[];
+  float* ringA = smem_sb;
+  float* stB = smem_sb + SA * P::ATILE;  // two B stages, one per B group
+  __shared__ __align__(8) uint64_t fullA[SA], fullB[2], regionfree[MAXT];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t G = gridDim.x, c = blockIdx.x;
+  const uint32_t nt = (P::NTILES - c + G - 1) / G;
+  if (nt == 0 || nt > MAXT) return;
+  if (tid == 0) {
+    for (int s = 0; s < SA; ++s) mbar_init_cta(&fullA[s], 1);
+    mbar_init_cta(&fullB[0], 1);
+    mbar_init_cta(&fullB[1], 1);
+    for (int k = 0; k < MAXT; ++k) mbar_init_cta(&regionfree[k], 2);  // both B groups
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t total = rows * nt;
+  float v[64];
+  if (tid < (uint32_t)P::NTA) {  // ---- A group (8 warps)
+    const uint32_t gt = tid;
+    auto bar = [] { named_bar(1, P::NTA); };
+    uint64_t pol = 0;
+    auto issue = [&](uint32_t u) {
+      const uint32_t r = u / nt, i = u - r * nt;
+      const int st = (int)(u % SA);
+      mbar_expect_tx_cta(&fullA[st], TBA);
+      const uint64_t a = c + (uint64_t)i * G;
+      bulk_g2s(ringA + st * P::ATILE, in + ((uint64_t)r << 24) + (a << 14), TBA, &fullA[st], pol);
+    };
+    if (gt == 0) {
+      pol = l2_evict_first_policy();
+      for (uint32_t u = 0; u < (uint32_t)SA && u < total; ++u) issue(u);
+    }
+    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
+      const int st = (int)(u % SA);
+      float* stage = ringA + st * P::ATILE;
+      uint32_t gtv = gt;
+      asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
+      mbar_wait_cta(&fullA[st], (u / SA) & 1u);
+      smem_load<P::AL0, NoSwz>(stage, v, gtv);
+      butterflies<P::AL0, P::AB0, false>(v);
+      bar();
+      smem_store<P::AL0, P::AS1>(stage, v, gtv);
+      bar();
+      smem_load<P::AL1, P::AS1>(stage, v, gtv);
+      butterflies<P::AL1, P::AB1, false>(v);
+      bar();
+      smem_store<P::AL1, P::AS2>(stage, v, gtv);
+      bar();
+      smem_load<P::AL2, P::AS2>(stage, v, gtv);
+      bar();  // every thread has read the stage: refill it
+      if (gt == 0 && u + SA < total) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(u + SA);
+      }
+      butterflies<P::AL2, P::AB2, false>(v);
+      if (r >= 1) mbar_wait_cta(&regionfree[i], (r - 1) & 1u);  // both B(r-1, .) tiles read
+      const uint32_t a = c + i * G;
+      if (r & 1u)
+        store_global<P::AL2, P::AOutQ, false, Cache::kL2>(ws + ((uint64_t)a << 3), v, gtv, 1.0f);
+      else
+        store_global<P::AL2, P::AOutP, false, Cache::kL2>(ws + ((uint64_t)a << 14), v, gtv, 1.0f);
+      if (i + 1 == nt) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        bar();
+        if (gt == 0) red_release_add(&cnt[r], nt);
+      }
+    }
+  } else {  // ---- B groups (4 warps each)
+    const uint32_t g = (tid - P::NTA) / P::NTB;
+    const uint32_t gt = (tid - P::NTA) % P::NTB;
+    const uint32_t barid = 2 + g;
+    auto bar = [barid] { named_bar(barid, P::NTB); };
+    float* stage = stB + g * P::BTILE;
+    uint64_t pol = 0;
+    auto tile_of = [&](uint32_t r, uint32_t i) -> uint32_t {
+      const uint32_t a = c + i * G;
+      return (r & 1u) ? 2 * a + g : a + 1024 * g;
+    };
+    auto issue = [&](uint32_t u, bool wait) -> bool {
+      const uint32_t r = u / nt, i = u - r * nt;
+      if (i == 0) {
+        if (ld_relaxed_u32(&cnt[r]) < P::NTILES) {
+          if (!wait) return false;
+          while (ld_relaxed_u32(&cnt[r]) < P::NTILES) __nanosleep(64);
+        }
+        (void)ld_acquire_gpu_u32(&cnt[r]);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      mbar_expect_tx_cta(&fullB[g], TBB);
+      const uint32_t t = tile_of(r, i);
+      if (r & 1u)
+        bulk_g2s(stage, ws + ((uint64_t)t << 13), TBB, &fullB[g], pol);
+      else
+        tensor4_g2s_hint(stage, &tmapP, 0, (int)t, 0, 0, &fullB[g], pol);
+      return true;
+    };
+    bool pending = false;
+    if (gt == 0) {
+      pol = l2_evict_normal_policy();
+      pending = total > 0;
+    }
+    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
+      if (pending) pending = !issue(u, true);
+      uint32_t gtv = gt;
+      asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
+      mbar_wait_cta(&fullB[g], u & 1u);
+      if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
+      smem_load<P::BL0, NoSwz>(stage, v, gtv);
+      butterflies<P::BL0, P::BB0, false>(v);
+      bar();
+      smem_store<P::BL0, P::BS1>(stage, v, gtv);
+      bar();
+      smem_load<P::BL1, P::BS1>(stage, v, gtv);
+      butterflies<P::BL1, P::BB1, false>(v);
+      bar();
+      smem_store<P::BL1, P::BS2>(stage, v, gtv);
+      bar();
+      smem_load<P::BL2, P::BS2>(stage, v, gtv);
+      bar();  // the stage is free: load this group's next B tile
+      if (gt == 0 && u + 1 < total) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        pending = !issue(u + 1, false);
+      }
+      butterflies<P::BL2, P::BB2, false>(v);
+      const uint32_t t = tile_of(r, i);
+      store_global<P::BL2, P::BOut, SCALE, Cache::kStream>(out + ((uint64_t)r << 24) + deposit<P::BOuter>(t), v,
+                                                            gtv, scale);
     }
   }
 }
