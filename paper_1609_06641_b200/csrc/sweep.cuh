@@ -41,6 +41,11 @@
 #endif
 // Debug builds (-DCHW_SWEEP_TRACE=1, tools/sweep_trace.py) record %globaltimer
 // stamps per tile for CTAs 0 and 1: [cta][group][item][event].
+// Passengers j2, j3 butterflied by B instead of A (A 12 bits, B 12 bits):
+// same-box A/B 0.546 / 0.546 vs 0.526 / 0.526 (profiles/r02_ab_sweep_rebal.txt).
+#ifndef CHW_SWEEP_REBAL
+#define CHW_SWEEP_REBAL 1
+#endif
 #ifndef CHW_SWEEP_TRACE
 #define CHW_SWEEP_TRACE 0
 #endif
@@ -57,7 +62,12 @@ struct SweepF32M24 {
   using AL1 = Layout<BL<2, 3, 4, 10, 11, 12, 13>, BL<5, 6, 0, 1, 7, 8, 9>>;
   using AS = Swz<5, 2, 6, 3, 7, 4>;
   using AB0 = BL<0, 1, 5, 6, 7, 8, 9>;
+#if CHW_SWEEP_REBAL
+  // passengers j2, j3 are butterflied by B (register bits t0, t1 of BL0)
+  using AB1 = BL<4, 10, 11, 12, 13>;
+#else
   using AB1 = BL<2, 3, 4, 10, 11, 12, 13>;
+#endif
   // workspace position of tile bit k: passengers j2,j3,j5,j6 -> addr 0..3;
   // v bits (j0,j1,j7,j8,j9,j4,j10..13) -> addr 4..13 (P) or 14..23 (Q).
   using AOutP = ListMap<4, 5, 0, 1, 9, 2, 3, 6, 7, 8, 10, 11, 12, 13>;         // tile base a << 14
@@ -66,7 +76,11 @@ struct SweepF32M24 {
   using BL0 = Layout<BL<0, 1, 7, 8, 9, 10, 11>, BL<2, 3, 4, 5, 6, 12, 13>>;
   using BL1 = Layout<BL<13, 12, 4, 5, 6, 0, 1>, BL<11, 10, 9, 8, 7, 2, 3>>;
   using BS = Swz<9, 2, 10, 3, 11, 4>;
+#if CHW_SWEEP_REBAL
+  using BB0 = BL<0, 1, 7, 8, 9, 10, 11>;
+#else
   using BB0 = BL<7, 8, 9, 10, 11>;
+#endif
   using BB1 = BL<4, 5, 6, 12, 13>;
   // The B transpose goes through a 32 KiB buffer in two halves (t0 = 0, 1):
   // the same layouts with tile bit t0 removed (tile bits renumbered t1 -> 0,
