@@ -224,12 +224,20 @@ size_t workspace_for(chw_dtype dtype, int64_t batch, int m) {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 int k1max_of(chw_dtype dtype);
+// NATURAL and SEQUENCY are folded into the single-pass kernels' stores.
+bool order_fused(chw_dtype dtype, int m, chw_order order) {
+  if (order == CHW_ORDER_DYADIC) return true;
+  if (m <= k1max_of(dtype)) return true;
+  // sequency is an XOR-linear map of the dyadic position: folded into the
+  // f32 long-row kernels' stores (K6 m = 16, K9 m = 24)
+  return order == CHW_ORDER_SEQUENCY && dtype == CHW_F32 && (m == 16 || m == 24);
+}
 
 size_t ordered_workspace(chw_dtype dtype, int64_t batch, int m, chw_order order) {
   const size_t inner = workspace_for(dtype, batch, m);
   if (order == CHW_ORDER_DYADIC || batch <= 0) return inner;
-  // Natural order on single-pass sizes is the kernel's store map: no gather buffer.
-  if (order == CHW_ORDER_NATURAL && m <= k1max_of(dtype)) return inner;
+  // Orders folded into the kernel's store map need no gather buffer.
+  if (order_fused(dtype, m, order)) return inner;
   return align256(inner) + (size_t)batch * ((size_t)1 << m) * elem_size(dtype);
 }
 
@@ -246,21 +254,21 @@ int k1max_of(chw_dtype dtype) {
   return -1;
 }
 
-chw_status natural_k1_impl(const void* in, void* out, chw_dtype dtype, int64_t batch, int m, chw_mode mode,
-                           cudaStream_t st) {
+chw_status ordered_k1_impl(const void* in, void* out, chw_dtype dtype, int64_t batch, int m, chw_mode mode,
+                           bool seq, cudaStream_t st) {
   const bool ortho = (mode == CHW_ORTHONORMAL);
   switch (dtype) {
     case CHW_F64:
-      return forward_k1_natural<double>(m, ortho, static_cast<const double*>(in), static_cast<double*>(out),
+      return forward_k1_natural<double>(m, ortho, seq, static_cast<const double*>(in), static_cast<double*>(out),
                                         batch, 1.0, st);
     case CHW_I64:
-      return forward_k1_natural<long long>(m, false, static_cast<const long long*>(in),
+      return forward_k1_natural<long long>(m, false, seq, static_cast<const long long*>(in),
                                            static_cast<long long*>(out), batch, 1, st);
     case CHW_F32:
-      return forward_k1_natural<float>(m, ortho, static_cast<const float*>(in), static_cast<float*>(out), batch,
+      return forward_k1_natural<float>(m, ortho, seq, static_cast<const float*>(in), static_cast<float*>(out), batch,
                                        (float)ortho_scale(m), st);
     case CHW_BF16:
-      return forward_k1_natural<__nv_bfloat16>(m, ortho, static_cast<const __nv_bfloat16*>(in),
+      return forward_k1_natural<__nv_bfloat16>(m, ortho, seq, static_cast<const __nv_bfloat16*>(in),
                                                static_cast<__nv_bfloat16*>(out), batch, (float)ortho_scale(m),
                                                st);
   }
@@ -283,8 +291,18 @@ chw_status forward_impl(const void* in, void* out, chw_dtype dtype, int64_t batc
   if (chw_status s = lease_workspace("chw_forward", need, workspace, workspace_bytes, st, &lease)) return s;
   void* ws = lease.p;
   if (order == CHW_ORDER_DYADIC) return dyadic_impl(in, out, dtype, batch, m, mode, ws, st);
-  // Natural order for single-pass sizes: the order is the kernel's store map.
-  if (order == CHW_ORDER_NATURAL && m <= k1max_of(dtype)) return natural_k1_impl(in, out, dtype, batch, m, mode, st);
+  // Natural / sequency order for single-pass sizes: the order is the kernel's
+  // store map (identity / inverse Gray code), zero extra bytes.
+  if (m <= k1max_of(dtype))
+    return ordered_k1_impl(in, out, dtype, batch, m, mode, order == CHW_ORDER_SEQUENCY, st);
+  if (order_fused(dtype, m, order)) {  // f32 sequency at m = 16 / 24
+    const bool ortho = (mode == CHW_ORTHONORMAL);
+    const float sc = (float)ortho_scale(m);
+    auto* i = static_cast<const float*>(in);
+    auto* o = static_cast<float*>(out);
+    if (m == 16) return launch_rowpipe_m16_seq(ortho, i, o, ws, batch, sc, st);
+    return launch_sweep_m24(ortho, i, o, ws, batch, sc, st, true);
+  }
   // Other orders: dyadic result into the workspace, then one coalesced gather.
   void* tmp = static_cast<char*>(ws) + align256(workspace_for(dtype, batch, m));
   if (chw_status s = dyadic_impl(in, tmp, dtype, batch, m, mode, ws, st)) return s;

@@ -98,6 +98,34 @@ struct RevMap {
   CHW_HD static constexpr int pos(int k) { return k < M ? M - 1 - k : k; }
 };
 
+// Sequency output order (orderings.hpp:82-102): out[s] =
+// dyadic[gray(s)], i.e. the element at dyadic in-row position p is stored at
+// gray^-1(p) = p ^ p>>1 ^ p>>2 ^ ... — a GF(2)-linear map of the position, not
+// a bit permutation.  A map with kLinear applies lin() to the position that
+// Base::pos() gives; lin() is linear (XOR-additive), so a store address is
+// lin(thread part ^ tile-outer part) ^ lin(register part): one runtime value
+// per thread and a compile-time constant per register (stores are scalar:
+// the low address bits depend on every position bit).
+template <class Base, int M>
+struct SeqMap {
+  static constexpr bool kLinear = true;
+  CHW_HD static constexpr int pos(int k) { return Base::pos(k); }
+  CHW_HD static constexpr uint32_t lin(uint32_t p) {
+    const uint32_t mask = M >= 32 ? 0xffffffffu : ((1u << M) - 1u);
+    uint32_t lo = p & mask;
+    lo ^= lo >> 1;
+    lo ^= lo >> 2;
+    lo ^= lo >> 4;
+    lo ^= lo >> 8;
+    lo ^= lo >> 16;
+    return lo | (p & ~mask);
+  }
+};
+template <class Map, class = void>
+struct IsLinearMap : std::false_type {};
+template <class Map>
+struct IsLinearMap<Map, std::void_t<decltype(Map::kLinear)>> : std::integral_constant<bool, Map::kLinear> {};
+
 template <class L, class Map>
 CHW_HD constexpr uint32_t reg_off(int r) {
   uint32_t o = 0;
@@ -607,49 +635,80 @@ __device__ __forceinline__ void load_global_pred(const T* __restrict__ base, C (
   }
 }
 
-// Store a tile to global memory, multiplying by `scale` when SCALE.
+// Store a tile to global memory, multiplying by `scale` when SCALE.  `outer`
+// is the position of the tile's fixed (non-tile) bits inside the row: added
+// to the address for bit-permutation maps, folded through lin() for linear
+// maps (SeqMap).
 template <class L, class Map, bool SCALE, Cache CO = Cache::kNC, class T, class C>
 __device__ __forceinline__ void store_global(T* __restrict__ base, const C (&v)[L::E], uint32_t tid,
-                                             C scale) {
-  constexpr int VB = vec_bits<L, Map>(IoTraits<T>::VMAX);
-  const uint32_t tb = thr_off<L, Map>(tid);
-  static_for<L::E>([&](auto R) {
-    constexpr int r = decltype(R)::value;
-    if constexpr (vec_head<L, Map>(r, VB)) {
-      constexpr uint32_t ro = reg_off<L, Map>(r);
-      C tmp[1 << VB];
-      static_for<(1 << VB)>([&](auto Q) {
-        constexpr int q = decltype(Q)::value;
-        tmp[q] = v[vec_elem<L, Map>(r, q, VB)];
-      });
-      if constexpr (SCALE) {
-        if constexpr (std::is_same<C, float>::value && VB >= 1) {
-          static_for<(1 << VB) / 2>([&](auto Q) { mul2(tmp[2 * decltype(Q)::value], tmp[2 * decltype(Q)::value + 1], scale); });
-        } else {
-          static_for<(1 << VB)>([&](auto Q) { tmp[decltype(Q)::value] *= scale; });
+                                             C scale, uint32_t outer = 0) {
+  if constexpr (IsLinearMap<Map>::value) {
+    const uint32_t tb = Map::lin(thr_off<L, Map>(tid) ^ outer);
+    static_for<L::E>([&](auto R) {
+      constexpr int r = decltype(R)::value;
+      constexpr uint32_t ro = Map::lin(reg_off<L, Map>(r));
+      C tmp[1] = {v[r]};
+      if constexpr (SCALE) tmp[0] *= scale;
+      VecIO<T, 0, CO>::st(base + (tb ^ ro), tmp);
+    });
+  } else {
+    constexpr int VB = vec_bits<L, Map>(IoTraits<T>::VMAX);
+    const uint32_t tb = thr_off<L, Map>(tid) + outer;
+    static_for<L::E>([&](auto R) {
+      constexpr int r = decltype(R)::value;
+      if constexpr (vec_head<L, Map>(r, VB)) {
+        constexpr uint32_t ro = reg_off<L, Map>(r);
+        C tmp[1 << VB];
+        static_for<(1 << VB)>([&](auto Q) {
+          constexpr int q = decltype(Q)::value;
+          tmp[q] = v[vec_elem<L, Map>(r, q, VB)];
+        });
+        if constexpr (SCALE) {
+          if constexpr (std::is_same<C, float>::value && VB >= 1) {
+            static_for<(1 << VB) / 2>([&](auto Q) { mul2(tmp[2 * decltype(Q)::value], tmp[2 * decltype(Q)::value + 1], scale); });
+          } else {
+            static_for<(1 << VB)>([&](auto Q) { tmp[decltype(Q)::value] *= scale; });
+          }
         }
+        VecIO<T, VB, CO>::st(base + (tb + ro), tmp);
       }
-      VecIO<T, VB, CO>::st(base + (tb + ro), tmp);
-    }
-  });
+    });
+  }
 }
 
 template <class L, class Map, bool SCALE, class T, class C>
 __device__ __forceinline__ void store_global_pred(T* __restrict__ base, const C (&v)[L::E],
                                                   uint32_t tid, C scale, uint32_t limit) {
-  constexpr int VB = vec_bits<L, Map>(IoTraits<T>::VMAX);
-  const uint32_t tb = thr_off<L, Map>(tid);
+  // `limit` bounds the tile-local (pre-map) offset: the valid elements of a
+  // partial last tile are its first `limit` rows' worth of tile bits.
+  if constexpr (IsLinearMap<Map>::value) {
+    const uint32_t tp = thr_off<L, Map>(tid);
+    const uint32_t tb = Map::lin(tp);
+    static_for<L::E>([&](auto R) {
+      constexpr int r = decltype(R)::value;
+      constexpr uint32_t rp = reg_off<L, Map>(r);
+      constexpr uint32_t ro = Map::lin(rp);
+      if ((tp + rp) < limit) {
+        C tmp[1] = {v[r]};
+        if constexpr (SCALE) tmp[0] *= scale;
+        VecIO<T, 0>::st(base + (tb ^ ro), tmp);
+      }
+    });
+  } else {
+    constexpr int VB = vec_bits<L, Map>(IoTraits<T>::VMAX);
+    const uint32_t tb = thr_off<L, Map>(tid);
 #pragma unroll
-  for (int r = 0; r < L::E; ++r) {
-    if (!vec_head<L, Map>(r, VB)) continue;
-    C tmp[1 << VB];
+    for (int r = 0; r < L::E; ++r) {
+      if (!vec_head<L, Map>(r, VB)) continue;
+      C tmp[1 << VB];
 #pragma unroll
-    for (int q = 0; q < (1 << VB); ++q) {
-      const C x = v[vec_elem<L, Map>(r, q, VB)];
-      tmp[q] = SCALE ? x * scale : x;
+      for (int q = 0; q < (1 << VB); ++q) {
+        const C x = v[vec_elem<L, Map>(r, q, VB)];
+        tmp[q] = SCALE ? x * scale : x;
+      }
+      const uint32_t off = tb + reg_off<L, Map>(r);
+      if (off < limit) VecIO<T, VB>::st(base + off, tmp);
     }
-    const uint32_t off = tb + reg_off<L, Map>(r);
-    if (off < limit) VecIO<T, VB>::st(base + off, tmp);
   }
 }
 

@@ -203,14 +203,20 @@ chw_status launch_k1_nat(const T* in, T* out, int64_t batch, typename IoTraits<T
   }
   return CHW_OK;
 }
+// Output order of the single-pass plan's store map: NATURAL = identity
+// (fwht_natural), SEQUENCY = inverse Gray code of the dyadic position
+// (apply_permutation(dyadic_to_sequency)) — both folded into the stores.
 template <class T, Scaling SC, int M, int MHI>
-chw_status dispatch_range_nat(int m, const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale,
+chw_status dispatch_range_nat(int m, bool seq, const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale,
                               cudaStream_t st) {
   if constexpr (M > MHI) {
     return fail(CHW_ERR_UNSUPPORTED, "chw_forward: unsupported length");
   } else {
-    if (m == M) return launch_k1_nat<T, M, SC>(in, out, batch, scale, st);
-    return dispatch_range_nat<T, SC, M + 1, MHI>(m, in, out, batch, scale, st);
+    if (m == M) {
+      if (seq) return launch_k1_nat<T, M, SC, SeqMap<RevMap<M>, M>>(in, out, batch, scale, st);
+      return launch_k1_nat<T, M, SC>(in, out, batch, scale, st);
+    }
+    return dispatch_range_nat<T, SC, M + 1, MHI>(m, seq, in, out, batch, scale, st);
   }
 }
 
@@ -328,10 +334,10 @@ inline chw_status rowpipe_tmaps(void* ws, int ctas, TmapParam* t0, TmapParam* t1
   return CHW_OK;
 }
 
-template <bool SCALE, int SA, int SB, int HINT>
+template <bool SCALE, int SA, int SB, int HINT, bool SEQ = false>
 chw_status launch_rowpipe_ws4_m16_x(const float* in, float* out, void* ws, int64_t batch, float scale,
                                     cudaStream_t st) {
-  using P = RowPipeF32M16<HINT>;
+  using P = RowPipeF32M16<HINT, SEQ>;
   constexpr auto k = rowpipe_ws4_kernel<P, SA, SB, SCALE>;
   if (((uintptr_t)in | (uintptr_t)out | (uintptr_t)ws) & 15u)
     return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers and workspace must be 16-byte aligned");
@@ -383,9 +389,12 @@ inline char m24_mode() {
 inline size_t sweep_m24_workspace(int64_t batch) {
   return ((size_t)64 << 20) + (((size_t)std::max<int64_t>(batch, 0) * 4 + 255) & ~(size_t)255);
 }
-// K9 launcher (sweep.cu, its own translation unit).
+// K9 launcher (sweep.cu, its own translation unit); seq: sequency output order.
 chw_status launch_sweep_m24(bool scale_mode, const float* in, float* out, void* ws, int64_t batch, float scale,
-                            cudaStream_t st);
+                            cudaStream_t st, bool seq = false);
+// Sequency order folded into the f32 m = 16 (K6, inst_f32_m16.cu) store map.
+chw_status launch_rowpipe_m16_seq(bool scale_mode, const float* in, float* out, void* ws, int64_t batch,
+                                  float scale, cudaStream_t st);
 
 // K4T (passtma.cuh): the K4P two-pass schedule fed by TMA, in-place tile
 // transposes (3 tiles in flight per SM).  Same-box A/B: 42.8-42.9 % vs K4P
@@ -511,7 +520,7 @@ template <class T>
 chw_status forward_k1(int m, bool scaled_mode, const T* in, T* out, int64_t batch,
                       typename IoTraits<T>::C scale, cudaStream_t st);
 template <class T>
-chw_status forward_k1_natural(int m, bool scaled_mode, const T* in, T* out, int64_t batch,
+chw_status forward_k1_natural(int m, bool scaled_mode, bool seq, const T* in, T* out, int64_t batch,
                               typename IoTraits<T>::C scale, cudaStream_t st);
 template <class T>
 chw_status forward_k4(int m, bool scaled_mode, const T* in, T* out, void* ws, int64_t batch,
@@ -542,14 +551,14 @@ struct ModeScaling {
                                                                    scale, st);                   \
   }                                                                                             \
   template <>                                                                                  \
-  chw_status forward_k1_natural<T>(int m, bool scaled_mode, const T* in, T* out, int64_t batch, \
+  chw_status forward_k1_natural<T>(int m, bool scaled_mode, bool seq, const T* in, T* out, int64_t batch, \
                                    typename IoTraits<T>::C scale, cudaStream_t st) {            \
     if constexpr (!std::is_same<T, long long>::value) {                                         \
       if (scaled_mode)                                                                          \
-        return dispatch_range_nat<T, ModeScaling<T>::kOrtho, 0, Regime<T>::K1MAX>(m, in, out,   \
+        return dispatch_range_nat<T, ModeScaling<T>::kOrtho, 0, Regime<T>::K1MAX>(m, seq, in, out, \
                                                                                   batch, scale, st); \
     }                                                                                           \
-    return dispatch_range_nat<T, Scaling::kNone, 0, Regime<T>::K1MAX>(m, in, out, batch, scale, st); \
+    return dispatch_range_nat<T, Scaling::kNone, 0, Regime<T>::K1MAX>(m, seq, in, out, batch, scale, st); \
   }
 
 #define CHW_INSTANTIATE_K4(T)                                                                  \

@@ -69,11 +69,11 @@ struct TwoPhase {
   }
   template <bool SCALE, class TOut>
   __device__ __forceinline__ static void phase1(const float* work, TOut* gout, float (&v)[E], uint32_t tid,
-                                                float scale) {
+                                                float scale, uint32_t outer = 0) {
     smem_load<L1, S>(work, v, tid);
     butterflies<L1, B1_, false>(v);
     if constexpr (SHFL_ >= 0) shfl_butterfly<L1, SHFL_, false>(v, tid);
-    store_global<L1, MapOut, SCALE, COUT_>(gout, v, tid, scale);
+    store_global<L1, MapOut, SCALE, COUT_>(gout, v, tid, scale, outer);
   }
 };
 

@@ -39,7 +39,7 @@ __device__ __forceinline__ void discard_l2_128(const void* p) {
 // HINT bit 0: workspace stores evict_last, input loads evict_first.
 // HINT bit 1: before a layout-0 A tile overwrites its contiguous 16 KiB
 //             workspace region, discard the region's dead lines (no write-back).
-template <int HINT_>
+template <int HINT_, bool SEQ = false>
 struct RowPipeF32M16 {
   using F = FusedF32M16b;
   static constexpr int M = 16;
@@ -62,7 +62,9 @@ struct RowPipeF32M16 {
   using BL0 = Layout<BL<0, 1, 5, 8, 9>, BL<2, 3, 4, 6, 7, 10, 11>>;
   using BL1 = Layout<BL<4, 6, 7, 10, 11>, BL<9, 8, 5, 0, 1, 2, 3>>;
   using BS = Swz<5, 2, 8, 3, 9, 4>;
-  using ItemB0 = TwoPhase<BL0, BL1, BS, BL<5, 8, 9>, BL<4, 6, 7, 10, 11>, -1, F::B::MapIn, F::B::MapOut,
+  // SEQ: sequency order (inverse Gray code of the dyadic position, f2).
+  using MapOutB = typename std::conditional<SEQ, SeqMap<F::B::MapOut, 16>, F::B::MapOut>::type;
+  using ItemB0 = TwoPhase<BL0, BL1, BS, BL<5, 8, 9>, BL<4, 6, 7, 10, 11>, -1, F::B::MapIn, MapOutB,
                           Cache::kStream>;
   static constexpr int TILE = ItemA0::TILE;
   static_assert(TILE == ItemB0::TILE && ItemA0::E == ItemB0::E, "A and B tiles must match");
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(4 * P::NT + 64, 1)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[kk])) : "memory");
       }
       const uint64_t row = c + (uint64_t)i * G;
-      P::ItemB0::template phase1<SCALE>(work, out + row * n + deposit<P::F::B::OuterOut>(kk), v, gt, scale);
+      P::ItemB0::template phase1<SCALE>(work, out + row * n, v, gt, scale, deposit<P::F::B::OuterOut>(kk));
       named_bar(bar, NT);  // work tile free for the next phase0
     }
   }

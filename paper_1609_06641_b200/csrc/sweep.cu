@@ -22,10 +22,10 @@ chw_status sweep_tmap(float* ws, TmapParam* t) {
   return CHW_OK;
 }
 
-template <bool SCALE>
+template <bool SCALE, bool SEQ>
 chw_status launch_sweep_t(const float* in, float* out, void* ws, int64_t batch, float scale, cudaStream_t st) {
   using P = SweepF32M24;
-  constexpr auto k = sweep_m24_kernel<SCALE>;
+  constexpr auto k = sweep_m24_kernel<SCALE, SEQ>;
   constexpr int smem = 3 * P::TILE * 4 + P::TILE * 2;  // two A stages, one B stage, B transpose buffer
   if (((uintptr_t)in | (uintptr_t)out | (uintptr_t)ws) & 15u)
     return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers and workspace must be 16-byte aligned");
@@ -119,10 +119,13 @@ char sweep_variant() {
 }  // namespace
 
 chw_status launch_sweep_m24(bool scale_mode, const float* in, float* out, void* ws, int64_t batch, float scale,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool seq) {
+  if (seq)
+    return scale_mode ? launch_sweep_t<true, true>(in, out, ws, batch, scale, st)
+                      : launch_sweep_t<false, true>(in, out, ws, batch, scale, st);
   if (sweep_variant() == 'a')
-    return scale_mode ? launch_sweep_t<true>(in, out, ws, batch, scale, st)
-                      : launch_sweep_t<false>(in, out, ws, batch, scale, st);
+    return scale_mode ? launch_sweep_t<true, false>(in, out, ws, batch, scale, st)
+                      : launch_sweep_t<false, false>(in, out, ws, batch, scale, st);
   return scale_mode ? launch_sweep_b<true>(in, out, ws, batch, scale, st)
                     : launch_sweep_b<false>(in, out, ws, batch, scale, st);
 }

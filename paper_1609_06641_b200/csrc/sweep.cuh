@@ -185,7 +185,7 @@ __device__ __forceinline__ void trace_stamp(uint32_t cta, uint32_t grp, uint32_t
   } while (0)
 #endif
 
-template <bool SCALE>
+template <bool SCALE, bool SEQ = false>
 __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
     sweep_m24_kernel(const float* __restrict__ in, float* __restrict__ out, float* __restrict__ ws,
                      uint32_t* __restrict__ cnt, uint32_t rows, float scale, const __grid_constant__ TmapParam tmapP) {
@@ -323,7 +323,9 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       // never touches t0) and the stores run per half, so only 64 extra
       // registers are live.
       const uint32_t t = c + i * G;
-      float* orow = out + ((uint64_t)r << 24) + deposit<P::BOuter>(t);
+      float* orow = out + ((uint64_t)r << 24);
+      const uint32_t outer = deposit<P::BOuter>(t);
+      using MapO = typename std::conditional<SEQ, SeqMap<P::BOutH, 24>, P::BOutH>::type;
       float w[P::E / 2];
       smem_store_half<P::BH0, P::BHS, P::BL0_T0, 0>(bufB, v, gtv);
       bar();
@@ -331,11 +333,11 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       bar();
       smem_store_half<P::BH0, P::BHS, P::BL0_T0, 1>(bufB, v, gtv);
       butterflies<P::BH1, P::BHB1, false>(w);
-      store_global<P::BH1, P::BOutH, SCALE, Cache::kStream>(orow, w, gtv, scale);
+      store_global<P::BH1, MapO, SCALE, Cache::kStream>(orow, w, gtv, scale, outer);
       bar();
       smem_load_half<P::BH1, P::BHS>(bufB, w, gtv);
       butterflies<P::BH1, P::BHB1, false>(w);
-      store_global<P::BH1, P::BOutH, SCALE, Cache::kStream>(orow + (1u << 21), w, gtv, scale);
+      store_global<P::BH1, MapO, SCALE, Cache::kStream>(orow, w, gtv, scale, outer | (1u << 21));
       SWEEP_STAMP(1, 3);
     }
   }

@@ -421,6 +421,38 @@ def test_orders_bitexact(cuda, m):
         assert np.array_equal(seq.cpu().numpy().view(np.uint64), ref_dy[:, gray].view(np.uint64))
 
 
+@pytest.mark.parametrize("m,rows", [(2, 37), (7, 300), (12, 149), (13, 5), (16, 150), (24, 3)])
+def test_sequency_fused_f32(cuda, m, rows):
+    """f2: sequency order folded into the store map (inverse Gray code of the
+    dyadic position): bit-exact integer probe against the reference permutation
+    (orderings.hpp:82-102) on batches that leave partial tiles / CTAs with 0-3
+    rows, in place and out of place, and with no extra gather launch."""
+    import torch
+
+    chw = _chw()
+    rng = np.random.default_rng(1500 + m)
+    bound = 1 << max(0, 24 - m)
+    xi = rng.integers(-bound, bound + 1, size=(rows, 1 << m), dtype=np.int64)
+    dy = oracle.chw_batch(xi, U)
+    gray = np.array([i ^ (i >> 1) for i in range(1 << m)])
+    ref = dy[:, gray]
+    t = torch.from_numpy(xi).to(cuda).to(torch.float32)
+    out = torch.empty_like(t)
+    n_dy = chw.launch_count()
+    chw.chw_forward_batched_(t.clone(), chw.ScalingMode.Unnormalized)
+    n_dy = chw.launch_count() - n_dy
+    n_seq = chw.launch_count()
+    chw.chw_forward_batched_(t, chw.ScalingMode.Unnormalized, out=out, order=chw.ORDER_SEQUENCY)
+    n_seq = chw.launch_count() - n_seq
+    chw.chw_forward_batched_(t, chw.ScalingMode.Unnormalized, order=chw.ORDER_SEQUENCY)  # in place
+    torch.cuda.synchronize()
+    assert np.array_equal(out.to(torch.float64).cpu().numpy().astype(np.int64), ref)
+    assert np.array_equal(t.to(torch.float64).cpu().numpy().astype(np.int64), ref)
+    assert n_seq == n_dy, "sequency must not add a gather pass"
+    assert chw.workspace_bytes_ordered(chw.DTYPE_F32, rows, 1 << m, chw.ORDER_SEQUENCY) == \
+        chw.workspace_bytes(chw.DTYPE_F32, rows, 1 << m)
+
+
 @pytest.mark.parametrize("dt", ["f32", "bf16", "i64"])
 @pytest.mark.parametrize("m", [3, 10, 12, 16])
 def test_orders_other_dtypes(cuda, dt, m):
