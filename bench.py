@@ -435,6 +435,35 @@ def time_config(torch, chw, cfg, first, rows, dev, steps, warmup, soak_s=0.0, or
             "flush": flush is not None, "alg_bytes": 2 * rows * n * es}
 
 
+def copy_floor(torch, cfg, dev, steps):
+    """A plain device copy of the same bytes (torch copy_, one read + one
+    write) under the same L2 protocol: the practical floor for configs whose
+    whole job is a single small wave (cfg1: 16 MiB)."""
+    name, dt, rows, m, _ = CONFIGS[cfg]
+    nbytes = rows * (1 << m) * ELEM_BYTES[dt]
+    a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    b = torch.empty_like(a)
+    flush = clean = None
+    if 2 * nbytes < 4 * 126 * 2**20:
+        flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
+        clean = torch.ones(64 * 2**20, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        b.copy_(a)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(steps):
+        if flush is not None:
+            flush.zero_()
+            clean.sum()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    return statistics.mean(ms)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as tdist
@@ -553,8 +582,10 @@ def run_ours(args):
             rc = time_config(torch, chw, c, 0, crows, dev, max(10, args.steps), 3)
             ms = statistics.mean(rc["kern_ms"])
             pc = check_parity(torch, chw, c, rc["x"], rc["out"]) if not args.no_parity else None
+            cms = copy_floor(torch, c, dev, max(10, args.steps))
             per_config[c] = {
                 "workload": cn, "value": round(crows * (1 << cm) / (ms * 1e-3) / 1e9, 3), "unit": "Gelem/s",
+                "copy_same_bytes_ms": round(cms, 4), "frac_of_copy": round(cms / ms, 4),
                 "ms_per_step": round(ms, 4), "frac": round(rc["alg_bytes"] / (ms * 1e-3) / 1e9 / peak, 4),
                 "plan": chw.plan_name(DTYPE_CODE[cdt], 1 << cm), "l2_flush": rc["flush"],
                 "traffic": load_traffic(c),

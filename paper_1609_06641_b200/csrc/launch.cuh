@@ -220,13 +220,30 @@ chw_status dispatch_range_nat(int m, bool seq, const T* in, T* out, int64_t batc
   }
 }
 
+template <class Plan, class T, int M, Scaling SC>
+chw_status launch_k1_plan(const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale, cudaStream_t st);
+
+// Optional tensor-core block path for bf16 m = 7 (tc.cu; CHW_B200_TC=1).
+bool tc_bf16_m7_enabled();
+chw_status launch_tc_bf16_m7(bool scale_mode, const __nv_bfloat16* in, __nv_bfloat16* out, int64_t batch,
+                             float scale, cudaStream_t st);
+
 // Output-order variants of a plan are produced by swapping the output map.
 template <class T, int M, Scaling SC>
 chw_status launch_k1(const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale,
                      cudaStream_t st) {
   if constexpr (std::is_same<T, float>::value && M == 12)
     return launch_k1t<SC == Scaling::kDeferred>(in, out, batch, scale, st);
-  using Plan = typename K1Select<T, M>::Plan;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value && M == 7)
+    if (tc_bf16_m7_enabled()) return launch_tc_bf16_m7(SC == Scaling::kDeferred, in, out, batch, scale, st);
+  // (f64 m = 10, cfg1: EB 3/4/5 x 1/2/4 rows per CTA measured within noise
+  // of each other, 0.14-0.18 of HBM peak: a single 16 MiB wave is launch- and
+  // latency-bound; profiles/r02_ab_cfg1.txt)
+  return launch_k1_plan<typename K1Select<T, M>::Plan, T, M, SC>(in, out, batch, scale, st);
+}
+
+template <class Plan, class T, int M, Scaling SC>
+chw_status launch_k1_plan(const T* in, T* out, int64_t batch, typename IoTraits<T>::C scale, cudaStream_t st) {
   constexpr int TB = Plan::kTB;
   constexpr int ROWS_PER_TILE = 1 << (TB - M);
   const uint64_t full = (uint64_t)batch / ROWS_PER_TILE;
@@ -500,6 +517,8 @@ const char* plan_name_m(int m) {
     if (m != M) return plan_name_m<T, M + 1>(m);
     if constexpr (M <= Regime<T>::K1MAX) {
       if constexpr (std::is_same<T, float>::value && M == 12) return "k1t-tma";
+      if constexpr (std::is_same<T, __nv_bfloat16>::value && M == 7)
+        if (tc_bf16_m7_enabled()) return "k7tc-tcgen05";
       return K1Select<T, M>::kTuned ? "k1-tuned" : "k1-generic";
     } else if constexpr (std::is_same<T, float>::value && M == 16) {
       return "k6-rowpipe";

@@ -97,7 +97,7 @@ def test_op_tally_closed_form(m):
 def test_plan_selection():
     # defaults (no CHW_B200_* schedule overrides in the environment)
     assert chw.plan_name(chw.DTYPE_F32, 4096) == "k1t-tma"
-    assert chw.plan_name(chw.DTYPE_BF16, 128) == "k1-tuned"
+    assert chw.plan_name(chw.DTYPE_BF16, 128) == "k7tc-tcgen05"
     assert chw.plan_name(chw.DTYPE_F64, 1024).startswith("k1")
     assert chw.plan_name(chw.DTYPE_F32, 1 << 24) == "k9-row-sweep"
     assert chw.plan_name(chw.DTYPE_F32, 1 << 16) == "k6-rowpipe"
