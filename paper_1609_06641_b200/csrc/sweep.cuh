@@ -317,8 +317,9 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         pending = !issue(u + 1, false);
       }
+      SWEEP_STAMP(1, 4);
       butterflies<P::BL0, P::BB0, false>(v);
-      // L0 -> L1 through the 32 KiB buffer, t0 = 0 half then t0 = 1 half.
+      SWEEP_STAMP(1, 5);
       // L0 -> L1 through the 32 KiB buffer one t0-half at a time; B1 (which
       // never touches t0) and the stores run per half, so only 64 extra
       // registers are live.
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       smem_store_half<P::BH0, P::BHS, P::BL0_T0, 1>(bufB, v, gtv);
       butterflies<P::BH1, P::BHB1, false>(w);
       store_global<P::BH1, MapO, SCALE, Cache::kStream>(orow, w, gtv, scale, outer);
+      SWEEP_STAMP(1, 6);
       bar();
       smem_load_half<P::BH1, P::BHS>(bufB, w, gtv);
       butterflies<P::BH1, P::BHB1, false>(w);

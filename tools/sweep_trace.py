@@ -41,11 +41,16 @@ for cta in range(2):
     b_issue = B[:n, 1] - B[:n, 0]
     b_wait = B[:n, 2] - B[:n, 1]
     b_comp = B[:n, 3] - B[:n, 2]
+    b_l0 = B[:n, 4] - B[:n, 2]
+    b_b0 = B[:n, 5] - B[:n, 4]
+    b_h0 = B[:n, 6] - B[:n, 5]
+    b_h1 = B[:n, 3] - B[:n, 6]
     span = np.nanmax(B[:n, 3]) - np.nanmin(A[:n, 0])
     print(f"CTA {cta}: span {span:.1f} us for {rows} rows = {span / rows:.2f} us/row")
     for name, arr in [("A wait input", a_wait_in), ("A compute", a_comp), ("A wait regionfree", a_wait_rf),
                       ("A store+signal", a_store), ("B wait cnt/issue", b_issue), ("B wait data", b_wait),
-                      ("B compute+store", b_comp)]:
+                      ("B compute+store", b_comp), ("  B LDS L0+bar", b_l0), ("  B B0 bfly", b_b0),
+                      ("  B half0 T+B1+STG", b_h0), ("  B half1 T+B1+STG", b_h1)]:
         print(f"   {name:18s} mean {np.nanmean(arr):6.2f}  sum/row {np.nansum(arr) / rows:6.2f}")
     # per row: when B of row r starts (tile 0 data ready) vs when A of row r finished
     for r in range(min(rows, 4)):
