@@ -46,6 +46,23 @@
 #ifndef CHW_SWEEP_REBAL
 #define CHW_SWEEP_REBAL 1
 #endif
+// A tiles leave through shared memory and a TMA store (bulk for layout P,
+// tensor box for layout Q) instead of 32 STG.128 per thread.  Measured slower
+// (0.502 vs 0.535: the stage is held until the store has read it and two more
+// shared-memory passes per tile), so off (profiles/r02_ab_sweep_atma.txt).
+#ifndef CHW_SWEEP_ATMA
+#define CHW_SWEEP_ATMA 0
+#endif
+// B tiles come straight from L2 into registers (16-byte .cg loads, the next
+// tile prefetched into the freed registers halfway through the current one)
+// instead of a TMA copy + shared-memory read: two fewer shared-memory passes
+// per tile pair, and the freed 64 KiB stage becomes a third A stage.
+// Measured slower (0.464 vs 0.534, at 1965 MHz without power capping: the L2
+// latency is exposed and the extra live registers spill), so off
+// (profiles/r02_ab_sweep_bldg.txt).
+#ifndef CHW_SWEEP_BLDG
+#define CHW_SWEEP_BLDG 0
+#endif
 #ifndef CHW_SWEEP_TRACE
 #define CHW_SWEEP_TRACE 0
 #endif
@@ -82,6 +99,8 @@ struct SweepF32M24 {
   using BB0 = BL<7, 8, 9, 10, 11>;
 #endif
   using BB1 = BL<4, 5, 6, 12, 13>;
+  // B tile positions in a layout-P workspace (tile base v << 4); layout Q: IdMap (base v << 14).
+  using BInP = ListMap<0, 1, 2, 3, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23>;
   // The B transpose goes through a 32 KiB buffer in two halves (t0 = 0, 1):
   // the same layouts with tile bit t0 removed (tile bits renumbered t1 -> 0,
   // ..., t13 -> 12); 8-byte vectors on t1; conflict-free (tools/swz_search.py).
@@ -153,6 +172,32 @@ __device__ __forceinline__ void smem_load_half(const float* sm, float (&w)[E2], 
     }
   });
 }
+// Registers of layout L -> shared memory at the positions of Map (vectorized
+// like store_global): used to stage a tile in its global order for a TMA store.
+template <class L, class Map, int E>
+__device__ __forceinline__ void smem_store_map(float* sm, const float (&v)[E], uint32_t tid) {
+  constexpr int VB = vec_bits<L, Map>(2);
+  const uint32_t tb = thr_off<L, Map>(tid);
+  static_for<L::E>([&](auto R) {
+    constexpr int r = decltype(R)::value;
+    if constexpr (vec_head<L, Map>(r, VB)) {
+      constexpr uint32_t ro = reg_off<L, Map>(r);
+      float tmp[1 << VB];
+      static_for<(1 << VB)>([&](auto Q) { tmp[decltype(Q)::value] = v[vec_elem<L, Map>(r, decltype(Q)::value, VB)]; });
+      SmemVec<float, VB>::st(sm + (tb + ro), tmp);
+    }
+  });
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tensor4_s2g(const void* tmap, const void* ssrc, int x, int y, int z, int w) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(tmap),
+               "r"(smem_u32(ssrc)), "r"(x), "r"(y), "r"(z), "r"(w)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -193,12 +238,12 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
   constexpr int TILE = P::TILE;
   constexpr uint32_t TB = TILE * 4;
   constexpr int NT = P::NT;
-  constexpr int SA = 2;
+  constexpr int SA = CHW_SWEEP_BLDG ? 3 : 2;
   constexpr int MAXT = 8;  // tiles per CTA per row (ceil(1024 / 148) = 7)
   extern __shared__ __align__(128) float smem_sw[];
   float* ringA = smem_sw;
-  float* stageB = smem_sw + SA * TILE;
-  float* bufB = stageB + TILE;  // TILE / 2 floats: the B transpose buffer
+  float* stageB = smem_sw + SA * TILE;  // (unused with CHW_SWEEP_BLDG)
+  float* bufB = CHW_SWEEP_BLDG ? stageB : stageB + TILE;  // TILE / 2 floats: the B transpose buffer
   __shared__ __align__(8) uint64_t fullA[SA], fullB, regionfree[MAXT];
   const uint32_t tid = threadIdx.x;
   const uint32_t G = gridDim.x, c = blockIdx.x;
@@ -247,6 +292,32 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       smem_store<P::AL0, P::AS>(stage, v, gtv);
       bar();
       smem_load<P::AL1, P::AS>(stage, v, gtv);
+#if CHW_SWEEP_ATMA
+      butterflies<P::AL1, P::AB1, false>(v);
+      SWEEP_STAMP(0, 2);
+      if (r >= 1) mbar_wait_cta(&regionfree[i], (r - 1) & 1u);  // B(r-1, a) has been read
+      SWEEP_STAMP(0, 3);
+      bar();  // every thread has read the stage: stage the result in it (the
+              // region order: layout P's contiguous region = layout Q's box order)
+      smem_store_map<P::AL1, P::AOutP>(stage, v, gtv);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar();
+      if (gt == 0) {
+        const uint32_t a = c + i * G;
+        if (r & 1u)
+          tensor4_s2g(&tmapP, stage, 0, (int)a, 0, 0);  // layout Q: 1024 runs of 64 B
+        else
+          bulk_s2g(ws + ((uint64_t)a << 14), stage, TB);  // layout P: contiguous 64 KiB
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (u + SA < total) issue(u + SA);  // the store has read the stage: refill it
+        if (i + 1 == nt) {  // this CTA's last A tile of row r: publish all nt of them
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          red_release_add(&cnt[r], nt);
+        }
+      }
+#else
       bar();  // every thread has read the stage: refill it
       if (gt == 0 && u + SA < total) {
         // order the group's generic-proxy reads of the stage before the TMA write
@@ -267,11 +338,70 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
         bar();
         if (gt == 0) red_release_add(&cnt[r], nt);
       }
+#endif
       SWEEP_STAMP(0, 4);
     }
   } else {  // ---- B group
     const uint32_t gt = tid - NT;
     auto bar = [] { named_bar(2, NT); };
+#if CHW_SWEEP_BLDG
+    // Load B tile u (this thread's 128 values, layout BL0) from the L2-resident
+    // workspace.  The first tile of a row needs every A tile of that row: with
+    // wait = false the call returns false if they are not all counted yet, and
+    // the thread loads the tile at the top of the next iteration instead.
+    auto load = [&](uint32_t u, bool wait, uint32_t gtv) -> bool {
+      const uint32_t r = u / nt, i = u - r * nt;
+      if (i == 0) {
+        if (ld_acquire_gpu_u32(&cnt[r]) < P::NTILES) {
+          if (!wait) return false;
+          while (ld_relaxed_u32(&cnt[r]) < P::NTILES) __nanosleep(64);
+          (void)ld_acquire_gpu_u32(&cnt[r]);  // synchronizes with every A tile's release
+        }
+      }
+      const uint32_t t = c + i * G;
+      if (r & 1u)
+        load_global<P::BL0, IdMap, Cache::kL2>(ws + ((uint64_t)t << 14), v, gtv);
+      else
+        load_global<P::BL0, P::BInP, Cache::kL2>(ws + ((uint64_t)t << 4), v, gtv);
+      return true;
+    };
+    bool pending = total > 0;  // tile u not loaded yet
+    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
+      uint32_t gtv = gt;
+#if CHW_SWEEP_OPAQUE
+      asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
+#endif
+      SWEEP_STAMP(1, 0);
+      if (pending) load(u, true, gtv);
+      SWEEP_STAMP(1, 1);
+      butterflies<P::BL0, P::BB0, false>(v);  // every loaded value consumed
+      SWEEP_STAMP(1, 2);
+      const uint32_t t = c + i * G;
+      float* orow = out + ((uint64_t)r << 24);
+      const uint32_t outer = deposit<P::BOuter>(t);
+      using MapO = typename std::conditional<SEQ, SeqMap<P::BOutH, 24>, P::BOutH>::type;
+      float w[P::E / 2];
+      bar();  // previous tile's buffer reads are done
+      smem_store_half<P::BH0, P::BHS, P::BL0_T0, 0>(bufB, v, gtv);
+      bar();
+      // every thread's loads of B(r, t) have returned: A(r+1, t) may overwrite it
+      if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
+      smem_load_half<P::BH1, P::BHS>(bufB, w, gtv);
+      bar();
+      smem_store_half<P::BH0, P::BHS, P::BL0_T0, 1>(bufB, v, gtv);
+      // v is free: prefetch the next tile into it while this one finishes
+      pending = (u + 1 < total) ? !load(u + 1, false, gtv) : false;
+      SWEEP_STAMP(1, 4);
+      butterflies<P::BH1, P::BHB1, false>(w);
+      store_global<P::BH1, MapO, SCALE, Cache::kStream>(orow, w, gtv, scale, outer);
+      SWEEP_STAMP(1, 6);
+      bar();
+      smem_load_half<P::BH1, P::BHS>(bufB, w, gtv);
+      butterflies<P::BH1, P::BHB1, false>(w);
+      store_global<P::BH1, MapO, SCALE, Cache::kStream>(orow, w, gtv, scale, outer | (1u << 21));
+      SWEEP_STAMP(1, 3);
+    }
+#else
     uint64_t pol = 0;
     // Issue workspace tile u into the (free) B stage.  The first tile of a row
     // needs every A tile of that row: with wait = false the call returns
@@ -342,6 +472,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       store_global<P::BH1, MapO, SCALE, Cache::kStream>(orow, w, gtv, scale, outer | (1u << 21));
       SWEEP_STAMP(1, 3);
     }
+#endif
   }
 }
 
