@@ -63,6 +63,12 @@
 #ifndef CHW_SWEEP_BLDG
 #define CHW_SWEEP_BLDG 0
 #endif
+// Drop the dead L2 lines of consumed layout-Q B regions (discard.global.L2)
+// before A rewrites them.  Measured slower (0.522 vs 0.535,
+// profiles/r02_ab_sweep_discard.txt), so off.
+#ifndef CHW_SWEEP_DISCARD
+#define CHW_SWEEP_DISCARD 0
+#endif
 #ifndef CHW_SWEEP_TRACE
 #define CHW_SWEEP_TRACE 0
 #endif
@@ -439,10 +445,26 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
 #endif
       mbar_wait_cta(&fullB, u & 1u);
       SWEEP_STAMP(1, 2);
+#if CHW_SWEEP_DISCARD
+      // Layout-Q tiles are whole 64 KiB regions: drop their now-dead L2 lines
+      // (no write-back) instead of letting them be evicted dirty before
+      // A(r+1, t) rewrites them — before `regionfree` lets A write there.
+      // (Layout-P tiles share every 128-byte line with another CTA's tile.)
+      if (r & 1u) {
+        const float* reg = ws + ((uint64_t)(c + i * G) << 14);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) discard_l2_128(reg + (gt + q * NT) * 32u);
+      }
+#else
       // B(r, t)'s workspace bytes are in shared memory: A(r+1, t) may overwrite them.
       if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
+#endif
       smem_load<P::BL0, NoSwz>(stageB, v, gtv);
       bar();  // the stage is read: load the next B tile while this one is computed
+#if CHW_SWEEP_DISCARD
+      // every thread's discards are done: A(r+1, t) may overwrite the region
+      if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
+#endif
       if (gt == 0 && u + 1 < total) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         pending = !issue(u + 1, false);
