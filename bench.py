@@ -579,7 +579,7 @@ def run_ours(args):
             if c == cfg:
                 continue
             cn, cdt, crows, cm, _ = CONFIGS[c]
-            rc = time_config(torch, chw, c, 0, crows, dev, max(10, args.steps), 3)
+            rc = time_config(torch, chw, c, 0, crows, dev, max(10, args.steps), 3, soak_s=min(args.soak, 0.3))
             ms = statistics.mean(rc["kern_ms"])
             pc = check_parity(torch, chw, c, rc["x"], rc["out"]) if not args.no_parity else None
             cms = copy_floor(torch, c, dev, max(10, args.steps))

@@ -643,13 +643,44 @@ template <class L, class Map, bool SCALE, Cache CO = Cache::kNC, class T, class 
 __device__ __forceinline__ void store_global(T* __restrict__ base, const C (&v)[L::E], uint32_t tid,
                                              C scale, uint32_t outer = 0) {
   if constexpr (IsLinearMap<Map>::value) {
+    // When the position bits 0..VB-1 are register bits, the 2^VB values of a
+    // vector group land in one aligned 2^VB-element block (lin maps the low
+    // VB position bits into themselves), in an order fixed by the block's
+    // low address bits b: slot q holds the value whose lin() is q ^ b.  The
+    // thread permutes its registers with selects and issues one vector store.
+    constexpr int VB = vec_bits<L, Map>(IoTraits<T>::VMAX);
+    constexpr int NV = 1 << VB;
     const uint32_t tb = Map::lin(thr_off<L, Map>(tid) ^ outer);
     static_for<L::E>([&](auto R) {
       constexpr int r = decltype(R)::value;
-      constexpr uint32_t ro = Map::lin(reg_off<L, Map>(r));
-      C tmp[1] = {v[r]};
-      if constexpr (SCALE) tmp[0] *= scale;
-      VecIO<T, 0, CO>::st(base + (tb ^ ro), tmp);
+      if constexpr (vec_head<L, Map>(r, VB)) {
+        constexpr uint32_t ro = Map::lin(reg_off<L, Map>(r));
+        const uint32_t addr = tb ^ ro;
+        C e[NV];  // e[c]: the group's value whose low address bits (lin) are c
+        static_for<NV>([&](auto A) {
+          constexpr int a = decltype(A)::value;
+          constexpr int cidx = (int)(Map::lin((uint32_t)a) & (NV - 1));
+          e[cidx] = v[vec_elem<L, Map>(r, a, VB)];
+        });
+        C tmp[NV];
+        const uint32_t b = addr & (NV - 1);
+        static_for<NV>([&](auto Q) {
+          constexpr int q = decltype(Q)::value;
+          // tmp[q] = e[q ^ b] with b a runtime value: a select tree on b's bits
+          C s[NV];
+          static_for<NV>([&](auto K) { s[decltype(K)::value] = e[decltype(K)::value ^ q]; });
+          static_for<VB>([&](auto Bt) {
+            constexpr int bit = decltype(Bt)::value;
+            const bool on = (b >> bit) & 1u;
+            static_for<(NV >> (bit + 1))>([&](auto J) {
+              constexpr int j = decltype(J)::value;
+              s[j] = on ? s[j * 2 + 1] : s[j * 2];
+            });
+          });
+          tmp[q] = SCALE ? s[0] * scale : s[0];
+        });
+        VecIO<T, VB, CO>::st(base + (addr & ~(uint32_t)(NV - 1)), tmp);
+      }
     });
   } else {
     constexpr int VB = vec_bits<L, Map>(IoTraits<T>::VMAX);

@@ -351,10 +351,10 @@ inline chw_status rowpipe_tmaps(void* ws, int ctas, TmapParam* t0, TmapParam* t1
   return CHW_OK;
 }
 
-template <bool SCALE, int SA, int SB, int HINT, bool SEQ = false>
+template <bool SCALE, int SA, int SB, int HINT, int ORD = 0>
 chw_status launch_rowpipe_ws4_m16_x(const float* in, float* out, void* ws, int64_t batch, float scale,
                                     cudaStream_t st) {
-  using P = RowPipeF32M16<HINT, SEQ>;
+  using P = RowPipeF32M16<HINT, ORD>;
   constexpr auto k = rowpipe_ws4_kernel<P, SA, SB, SCALE>;
   if (((uintptr_t)in | (uintptr_t)out | (uintptr_t)ws) & 15u)
     return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers and workspace must be 16-byte aligned");
@@ -409,9 +409,10 @@ inline size_t sweep_m24_workspace(int64_t batch) {
 // K9 launcher (sweep.cu, its own translation unit); seq: sequency output order.
 chw_status launch_sweep_m24(bool scale_mode, const float* in, float* out, void* ws, int64_t batch, float scale,
                             cudaStream_t st, bool seq = false);
-// Sequency order folded into the f32 m = 16 (K6, inst_f32_m16.cu) store map.
-chw_status launch_rowpipe_m16_seq(bool scale_mode, const float* in, float* out, void* ws, int64_t batch,
-                                  float scale, cudaStream_t st);
+// Natural (order 1) / sequency (order 2) folded into the f32 m = 16 (K6,
+// inst_f32_m16.cu) store map.
+chw_status launch_rowpipe_m16_ordered(int order, bool scale_mode, const float* in, float* out, void* ws,
+                                      int64_t batch, float scale, cudaStream_t st);
 
 // K4T (passtma.cuh): the K4P two-pass schedule fed by TMA, in-place tile
 // transposes (3 tiles in flight per SM).  Same-box A/B: 42.8-42.9 % vs K4P

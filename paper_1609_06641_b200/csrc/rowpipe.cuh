@@ -39,7 +39,8 @@ __device__ __forceinline__ void discard_l2_128(const void* p) {
 // HINT bit 0: workspace stores evict_last, input loads evict_first.
 // HINT bit 1: before a layout-0 A tile overwrites its contiguous 16 KiB
 //             workspace region, discard the region's dead lines (no write-back).
-template <int HINT_, bool SEQ = false>
+// ORD: 0 dyadic, 1 natural, 2 sequency (chw_order).
+template <int HINT_, int ORD = 0>
 struct RowPipeF32M16 {
   using F = FusedF32M16b;
   static constexpr int M = 16;
@@ -62,8 +63,18 @@ struct RowPipeF32M16 {
   using BL0 = Layout<BL<0, 1, 5, 8, 9>, BL<2, 3, 4, 6, 7, 10, 11>>;
   using BL1 = Layout<BL<4, 6, 7, 10, 11>, BL<9, 8, 5, 0, 1, 2, 3>>;
   using BS = Swz<5, 2, 8, 3, 9, 4>;
-  // SEQ: sequency order (inverse Gray code of the dyadic position, f2).
-  using MapOutB = typename std::conditional<SEQ, SeqMap<F::B::MapOut, 16>, F::B::MapOut>::type;
+  // Output orders (f2).  Sequency: inverse Gray code of the dyadic position.
+  // Natural: position = j; the B tile's passengers are j0..j3 (workspace
+  // addr 0..3 = j2, j3, j0, j1), so every tile still writes whole 64-byte
+  // runs (scalar stores; the dyadic order's 16-byte vectors need the tile's
+  // butterfly bits low), and its index bits (addr 4..7 = j5, j6, j7, j4)
+  // place the tile.
+  using MapOutNat = ListMap<2, 3, 0, 1, 8, 9, 10, 11, 12, 13, 14, 15>;
+  using OuterOutNat = BL<5, 6, 7, 4>;
+  using MapOutB = typename std::conditional<
+      ORD == 2, SeqMap<F::B::MapOut, 16>,
+      typename std::conditional<ORD == 1, MapOutNat, F::B::MapOut>::type>::type;
+  using OuterOutB = typename std::conditional<ORD == 1, OuterOutNat, F::B::OuterOut>::type;
   using ItemB0 = TwoPhase<BL0, BL1, BS, BL<5, 8, 9>, BL<4, 6, 7, 10, 11>, -1, F::B::MapIn, MapOutB,
                           Cache::kStream>;
   static constexpr int TILE = ItemA0::TILE;
@@ -243,7 +254,7 @@ __global__ void __launch_bounds__(4 * P::NT + 64, 1)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[kk])) : "memory");
       }
       const uint64_t row = c + (uint64_t)i * G;
-      P::ItemB0::template phase1<SCALE>(work, out + row * n, v, gt, scale, deposit<P::F::B::OuterOut>(kk));
+      P::ItemB0::template phase1<SCALE>(work, out + row * n, v, gt, scale, deposit<typename P::OuterOutB>(kk));
       named_bar(bar, NT);  // work tile free for the next phase0
     }
   }

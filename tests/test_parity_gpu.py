@@ -453,6 +453,42 @@ def test_sequency_fused_f32(cuda, m, rows):
         chw.workspace_bytes(chw.DTYPE_F32, rows, 1 << m)
 
 
+@pytest.mark.parametrize("rows", [1, 3, 149, 150])
+def test_natural_fused_f32_m16(cuda, rows):
+    """f2: natural order folded into the m = 16 row pipeline (K6) — bit-exact
+    integer probe against the reference's fwht_natural order, in place and out
+    of place, no extra gather launch or workspace."""
+    import torch
+
+    chw = _chw()
+    m = 16
+    rng = np.random.default_rng(1600 + rows)
+    xi = rng.integers(-256, 257, size=(rows, 1 << m), dtype=np.int64)
+    dy = oracle.chw_batch(xi, U)
+    rev = np.array([oracle.bit_reverse(i, m) for i in range(1 << m)])
+    ref = dy[:, rev]
+    t = torch.from_numpy(xi).to(cuda).to(torch.float32)
+    out = torch.empty_like(t)
+    n_dy = chw.launch_count()
+    chw.chw_forward_batched_(t.clone(), chw.ScalingMode.Unnormalized)
+    n_dy = chw.launch_count() - n_dy
+    n_nat = chw.launch_count()
+    chw.chw_forward_batched_(t, chw.ScalingMode.Unnormalized, out=out, order=chw.ORDER_NATURAL)
+    n_nat = chw.launch_count() - n_nat
+    chw.chw_forward_batched_(t, chw.ScalingMode.Unnormalized, order=chw.ORDER_NATURAL)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.to(torch.float64).cpu().numpy().astype(np.int64), ref)
+    assert np.array_equal(t.to(torch.float64).cpu().numpy().astype(np.int64), ref)
+    assert n_nat == n_dy
+    # orthonormal f32 within tolerance of the reference natural FWHT
+    x = rng.uniform(-1, 1, size=(rows, 1 << m)).astype(np.float32)
+    tx = torch.from_numpy(x).to(cuda)
+    chw.chw_forward_batched_(tx, chw.ScalingMode.Orthonormal, order=chw.ORDER_NATURAL)
+    got = tx.cpu().numpy().astype(np.float64)
+    want = np.stack([oracle.simple("fwht_natural", x[r].astype(np.float64), O) for r in range(rows)])
+    assert _rel_l2(got, want) <= F32_TOL
+
+
 @pytest.mark.parametrize("dt", ["f32", "bf16", "i64"])
 @pytest.mark.parametrize("m", [3, 10, 12, 16])
 def test_orders_other_dtypes(cuda, dt, m):
