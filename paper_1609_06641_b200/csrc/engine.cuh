@@ -537,6 +537,24 @@ __device__ __forceinline__ void mul2(float& a, float& b, float s) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(P));
 }
 
+// The butterfly between the two halves of one register pair, (a, b) ->
+// (a + b, a - b), as ONE packed FFMA2: (b, b) * (1, -1) + (a, a).  ptxas folds
+// the broadcasts into operand modifiers (FFMA2 R, Rb.F32, Rc.F32x2, Ra.F32); a
+// product by +-1 is exact, so each half is rounded exactly like
+// __fadd_rn / __fsub_rn.  Used for register bit 0, which the (r, r|1) pairing
+// of the other bits cannot pack (64 scalar FADDs less per 128-value level).
+#ifndef CHW_BF_SELF
+#define CHW_BF_SELF 1
+#endif
+__device__ __forceinline__ void bf_self(float& a, float& b) {
+  uint64_t LL, HH, C, D;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(LL) : "f"(a));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(HH) : "f"(b));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(C) : "f"(1.0f), "f"(-1.0f));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(D) : "l"(HH), "l"(C), "l"(LL));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(D));
+}
+
 // Butterflies on the listed tile bits, in list order (order matters only for
 // bit-exact f64; f32/bf16 are order-free up to rounding).  fp32 butterflies on
 // register bits other than bit 0 are issued in pairs (registers r, r^1) as
@@ -553,12 +571,19 @@ __device__ __forceinline__ void butterflies(C (&v)[L::E]) {
           if constexpr (!((r >> k) & 1)) bf2(v[r], v[r | 1], v[r | (1 << k)], v[(r | (1 << k)) | 1]);
         });
       } else {
-        // register bit 0 stays scalar: pairing (r, r|2) for it would fight the
-        // (r, r|1) register pairs of every other bit (measured: the repacking
-        // MOVs cost more than the saved FADDs, cfg5 0.53 -> 0.49).
+        // register bit 0: the butterfly inside each (r, r|1) pair, one FFMA2
+        // (bf_self).  Pairing (r, r|2) for it instead fights the (r, r|1)
+        // pairs of every other bit (measured: the repacking MOVs cost more
+        // than the saved FADDs, cfg5 0.53 -> 0.49).
         static_for<L::E>([&](auto R) {
           constexpr int r = decltype(R)::value;
-          if constexpr (!((r >> k) & 1)) bf<PER_STAGE>(v[r], v[r | (1 << k)]);
+          if constexpr (!((r >> k) & 1)) {
+#if CHW_BF_SELF
+            bf_self(v[r], v[r | 1]);
+#else
+            bf<PER_STAGE>(v[r], v[r | (1 << k)]);
+#endif
+          }
         });
       }
     });

@@ -72,6 +72,12 @@
 #ifndef CHW_SWEEP_TRACE
 #define CHW_SWEEP_TRACE 0
 #endif
+// Diagnostic builds only (wrong results): 1 = the A group alone (no waits on B),
+// 2 = the B group alone (no waits on A) — each group's stand-alone tile rate
+// (profiles/r02_ab_sweep_only.txt).
+#ifndef CHW_SWEEP_ONLY
+#define CHW_SWEEP_ONLY 0
+#endif
 
 namespace chwb {
 
@@ -264,7 +270,8 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
   __syncthreads();
   const uint32_t total = rows * nt;  // A items (and B items) of this CTA
   float v[P::E];
-  if (tid < (uint32_t)NT) {  // ---- A group
+  if (tid < (uint32_t)NT && CHW_SWEEP_ONLY != 3) {  // ---- A group
+    if (CHW_SWEEP_ONLY == 2) return;
     const uint32_t gt = tid;
     auto bar = [] { named_bar(1, NT); };
     uint64_t pol = 0;
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       }
       butterflies<P::AL1, P::AB1, false>(v);
       SWEEP_STAMP(0, 2);
-      if (r >= 1) mbar_wait_cta(&regionfree[i], (r - 1) & 1u);  // B(r-1, a) has been read
+      if (CHW_SWEEP_ONLY != 1 && r >= 1) mbar_wait_cta(&regionfree[i], (r - 1) & 1u);  // B(r-1, a) has been read
       SWEEP_STAMP(0, 3);
       const uint32_t a = c + i * G;
       if (r & 1u)
@@ -348,8 +355,19 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       SWEEP_STAMP(0, 4);
     }
   } else {  // ---- B group
-    const uint32_t gt = tid - NT;
-    auto bar = [] { named_bar(2, NT); };
+    if (CHW_SWEEP_ONLY == 1) return;
+    // CHW_SWEEP_ONLY == 3 (diagnostic): both warp groups run the B path on
+    // alternate tiles, each with its own stage, buffer, mbarrier and barrier id.
+    const uint32_t bg = (CHW_SWEEP_ONLY == 3) ? tid / NT : 0u;
+    const uint32_t ustep = (CHW_SWEEP_ONLY == 3) ? 2u : 1u;
+    const uint32_t gt = (CHW_SWEEP_ONLY == 3) ? tid % NT : tid - NT;
+    if (CHW_SWEEP_ONLY == 3) {
+      stageB = smem_sw + bg * (TILE + TILE / 2);
+      bufB = stageB + TILE;
+    }
+    uint64_t* fullBp = (CHW_SWEEP_ONLY == 3) ? &fullA[bg] : &fullB;
+    const uint32_t barid = 2 + bg;
+    auto bar = [barid] { named_bar(barid, NT); };
 #if CHW_SWEEP_BLDG
     // Load B tile u (this thread's 128 values, layout BL0) from the L2-resident
     // workspace.  The first tile of a row needs every A tile of that row: with
@@ -414,7 +432,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
     // false instead of spinning, and the caller retries before it next waits.
     auto issue = [&](uint32_t u, bool wait) -> bool {
       const uint32_t r = u / nt, i = u - r * nt;
-      if (i == 0) {
+      if (CHW_SWEEP_ONLY < 2 && i == 0) {
         if (ld_relaxed_u32(&cnt[r]) < P::NTILES) {
           if (!wait) return false;
           while (ld_relaxed_u32(&cnt[r]) < P::NTILES) __nanosleep(64);
@@ -422,20 +440,22 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
         (void)ld_acquire_gpu_u32(&cnt[r]);  // synchronizes with every A tile's release
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
-      mbar_expect_tx_cta(&fullB, TB);
+      mbar_expect_tx_cta(fullBp, TB);
       const uint32_t t = c + i * G;
       if (r & 1u)
-        bulk_g2s(stageB, ws + ((uint64_t)t << 14), TB, &fullB, pol);
+        bulk_g2s(stageB, ws + ((uint64_t)t << 14), TB, fullBp, pol);
       else
-        tensor4_g2s_hint(stageB, &tmapP, 0, (int)t, 0, 0, &fullB, pol);
+        tensor4_g2s_hint(stageB, &tmapP, 0, (int)t, 0, 0, fullBp, pol);
       return true;
     };
     bool pending = false;  // thread 0: tile u not issued yet
     if (gt == 0) {
       pol = l2_evict_normal_policy();
-      pending = total > 0;
+      pending = total > bg;
     }
-    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
+    for (uint32_t u = bg, r = 0, i = bg; u < total; u += ustep) {
+      r = u / nt;
+      i = u - r * nt;
       SWEEP_STAMP(1, 0);
       if (pending) pending = !issue(u, true);
       SWEEP_STAMP(1, 1);
@@ -443,7 +463,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
 #if CHW_SWEEP_OPAQUE
       asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
 #endif
-      mbar_wait_cta(&fullB, u & 1u);
+      mbar_wait_cta(fullBp, (u / ustep) & 1u);
       SWEEP_STAMP(1, 2);
 #if CHW_SWEEP_DISCARD
       // Layout-Q tiles are whole 64 KiB regions: drop their now-dead L2 lines
@@ -457,7 +477,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       }
 #else
       // B(r, t)'s workspace bytes are in shared memory: A(r+1, t) may overwrite them.
-      if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
+      if (gt == 0 && CHW_SWEEP_ONLY != 3) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
 #endif
       smem_load<P::BL0, NoSwz>(stageB, v, gtv);
       bar();  // the stage is read: load the next B tile while this one is computed
@@ -465,9 +485,9 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       // every thread's discards are done: A(r+1, t) may overwrite the region
       if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
 #endif
-      if (gt == 0 && u + 1 < total) {
+      if (gt == 0 && u + ustep < total) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        pending = !issue(u + 1, false);
+        pending = !issue(u + ustep, false);
       }
       SWEEP_STAMP(1, 4);
       butterflies<P::BL0, P::BB0, false>(v);
