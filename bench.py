@@ -579,7 +579,13 @@ def run_ours(args):
             if c == cfg:
                 continue
             cn, cdt, crows, cm, _ = CONFIGS[c]
-            rc = time_config(torch, chw, c, 0, crows, dev, max(10, args.steps), 3, soak_s=min(args.soak, 0.3))
+            # same protocol as the main line: the full soak (after the CPU
+            # baseline the GPU has idled; a 0.3 s soak under-reported cfg2 by
+            # 10 %) and clocks sampled under load
+            csamp = ClockSampler(local_dev)
+            with csamp:
+                rc = time_config(torch, chw, c, 0, crows, dev, max(10, args.steps), max(3, args.warmup),
+                                 soak_s=args.soak)
             ms = statistics.mean(rc["kern_ms"])
             pc = check_parity(torch, chw, c, rc["x"], rc["out"]) if not args.no_parity else None
             cms = copy_floor(torch, c, dev, max(10, args.steps))
@@ -588,7 +594,7 @@ def run_ours(args):
                 "copy_same_bytes_ms": round(cms, 4), "frac_of_copy": round(cms / ms, 4),
                 "ms_per_step": round(ms, 4), "frac": round(rc["alg_bytes"] / (ms * 1e-3) / 1e9 / peak, 4),
                 "plan": chw.plan_name(DTYPE_CODE[cdt], 1 << cm), "l2_flush": rc["flush"],
-                "traffic": load_traffic(c),
+                "traffic": load_traffic(c), "clocks": csamp.summary(),
                 "parity": None if pc is None else {k: pc[k] for k in ("rows_checked", "max_rel_l2", "tolerance",
                                                                        "order_probe_ok", "ok")},
             }

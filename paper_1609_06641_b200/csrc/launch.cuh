@@ -18,6 +18,7 @@
 #include "fused.cuh"
 #include "pipelined.cuh"
 #include "rowpipe.cuh"
+#include "clusterm16.cuh"
 #include "k1t.cuh"
 #include "passtma.cuh"
 
@@ -381,6 +382,51 @@ chw_status launch_rowpipe_m16(const float* in, float* out, void* ws, int64_t bat
   return launch_rowpipe_ws4_m16_x<SCALE, 4, 6, 1>(in, out, ws, batch, scale, st);
 }
 
+// f32 m = 16 schedule: 'c' K10 cluster/DSMEM kernel (clusterm16.cuh), 'r' K6
+// row pipeline.
+inline char m16_mode() {
+  static const char mode = [] {
+    const char* e = std::getenv("CHW_B200_M16");
+    return (e && e[0] == 'c') ? 'c' : 'r';
+  }();
+  return mode;
+}
+// K10: clusters of 4 CTAs, one row per cluster at a time, no workspace.
+template <bool SCALE>
+chw_status launch_cluster_m16(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
+  using P = ClusterF32M16;
+  constexpr auto k = cluster_m16_kernel<SCALE>;
+  if (((uintptr_t)in | (uintptr_t)out) & 15u)
+    return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers and workspace must be 16-byte aligned");
+  if (batch > 0x7fffffffLL) return fail(CHW_ERR_UNSUPPORTED, "chw_forward: batch too large for the m = 16 cluster kernel");
+  constexpr int smem = (2 * P::TILE + 2 * (P::CL - 1) * (P::TILE / P::CL)) * 4;  // 2 buffers + 2 x 3 blocks
+  if (chw_status s = prep_kernel<k>(smem)) return s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P::CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(2 * P::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // persistent grid: as many clusters as can be resident (or one per row)
+  static std::atomic<int> max_clusters{0};
+  int ncl = max_clusters.load();
+  if (ncl <= 0) {
+    cfg.gridDim = dim3(P::CL * 64);
+    CHW_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
+    if (ncl <= 0) return fail(CHW_ERR_RESOURCE, "chw_forward: no room for a 4-CTA cluster (m = 16)");
+    max_clusters.store(ncl);
+  }
+  ncl = (int)std::min<int64_t>(ncl, batch);
+  cfg.gridDim = dim3((unsigned)(P::CL * ncl));
+  CHW_CUDA(cudaLaunchKernelEx(&cfg, k, in, out, (uint32_t)batch, scale));
+  return check_launch("cluster_m16_kernel");
+}
+
 // m = 24 (cfg5).  K4T: two statically scheduled passes through an HBM
 // intermediate in 16-row chunks (both passes TMA-fed).
 constexpr int64_t kM24Chunk = 16;  // rows per chunk: 1 GiB intermediate
@@ -490,6 +536,7 @@ chw_status launch_m(const T* in, T* out, void* ws, int64_t batch, typename IoTra
   if constexpr (M <= Regime<T>::K1MAX) {
     return launch_k1<T, M, SC>(in, out, batch, scale, st);
   } else if constexpr (std::is_same<T, float>::value && M == 16) {
+    if (m16_mode() == 'c') return launch_cluster_m16<SC == Scaling::kDeferred>(in, out, batch, scale, st);
     return launch_rowpipe_m16<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
   } else if constexpr (std::is_same<T, float>::value && M == 24) {
     if (m24_mode() == 's') return launch_sweep_m24(SC == Scaling::kDeferred, in, out, ws, batch, scale, st);
@@ -522,7 +569,7 @@ const char* plan_name_m(int m) {
         if (tc_bf16_m7_enabled()) return "k7tc-tcgen05";
       return K1Select<T, M>::kTuned ? "k1-tuned" : "k1-generic";
     } else if constexpr (std::is_same<T, float>::value && M == 16) {
-      return "k6-rowpipe";
+      return m16_mode() == 'c' ? "k10-cluster-dsmem" : "k6-rowpipe";
     } else if constexpr (std::is_same<T, float>::value && M == 24) {
       return m24_mode() == 's' ? "k9-row-sweep" : "k4t-two-pass-tma";
     } else {

@@ -36,6 +36,13 @@ def test_m16_rowpipe(cuda):
     assert "k6-rowpipe" in out
 
 
+def test_m16_cluster_dsmem(cuda):
+    """K10 (CHW_B200_M16=c): 4-CTA clusters, the row exchanged through
+    distributed shared memory; batches below, at and across the cluster count."""
+    out = _run({"CHW_B200_M16": "c"}, 16, [1, 2, 3, 5, 33, 67, 300, 445])
+    assert "k10-cluster-dsmem" in out
+
+
 def test_m16_default_is_rowpipe(cuda):
     env = {k: v for k, v in os.environ.items() if k != "CHW_B200_M16"}
     p = subprocess.run([sys.executable, os.path.join(REPO, "tools", "sched_check.py"), "--m", "16", "--rows", "5"],
