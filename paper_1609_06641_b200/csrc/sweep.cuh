@@ -78,6 +78,12 @@
 #ifndef CHW_SWEEP_ONLY
 #define CHW_SWEEP_ONLY 0
 #endif
+// Workspace cache hints: bit 0 = A's workspace stores carry an L2 evict_last
+// policy, bit 1 = B's workspace loads carry evict_first (the data is dead once
+// read).
+#ifndef CHW_SWEEP_WSHINT
+#define CHW_SWEEP_WSHINT 0
+#endif
 
 namespace chwb {
 
@@ -343,9 +349,11 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       SWEEP_STAMP(0, 3);
       const uint32_t a = c + i * G;
       if (r & 1u)
-        store_global<P::AL1, P::AOutQ, false, Cache::kL2>(ws + ((uint64_t)a << 4), v, gtv, 1.0f);
+        store_global<P::AL1, P::AOutQ, false, (CHW_SWEEP_WSHINT & 1) ? Cache::kL2Last : Cache::kL2>(
+            ws + ((uint64_t)a << 4), v, gtv, 1.0f);
       else
-        store_global<P::AL1, P::AOutP, false, Cache::kL2>(ws + ((uint64_t)a << 14), v, gtv, 1.0f);
+        store_global<P::AL1, P::AOutP, false, (CHW_SWEEP_WSHINT & 1) ? Cache::kL2Last : Cache::kL2>(
+            ws + ((uint64_t)a << 14), v, gtv, 1.0f);
       if (i + 1 == nt) {  // this CTA's last A tile of row r: publish all nt of them
         asm volatile("fence.proxy.async.global;" ::: "memory");  // other CTAs read them with TMA
         bar();
@@ -450,7 +458,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
     };
     bool pending = false;  // thread 0: tile u not issued yet
     if (gt == 0) {
-      pol = l2_evict_normal_policy();
+      pol = (CHW_SWEEP_WSHINT & 2) ? l2_evict_first_policy() : l2_evict_normal_policy();
       pending = total > bg;
     }
     for (uint32_t u = bg, r = 0, i = bg; u < total; u += ustep) {

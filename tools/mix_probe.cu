@@ -31,6 +31,14 @@ __device__ __forceinline__ float4 ld_cg(const float4* p) {
 __device__ __forceinline__ void st_cs(float4* p, float4 v) {
   asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
+__device__ __forceinline__ float4 ld_df(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_df(float4* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
 __device__ __forceinline__ void st_cg(float4* p, float4 v) {
   asm volatile("st.global.cg.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
@@ -40,14 +48,14 @@ __device__ __forceinline__ void st_cg(float4* p, float4 v) {
 // tile), chunks handed out round-robin over the role's CTAs.
 constexpr int UNROLL = 8;
 __global__ void __launch_bounds__(512) mix(const float4* __restrict__ in, float4* __restrict__ out,
-                                           float4* __restrict__ ws, size_t n4, size_t ws4, int mode) {
+                                           float4* __restrict__ ws, size_t n4, size_t ws4, int mode, int pol,
+                                           size_t chunk) {
   // mode 0: copy (all CTAs role 2); 1: A only; 2: B only; 3: mix (even CTAs A, odd CTAs B)
   int role, nrole, idx;
   if (mode == 0) { role = 2; nrole = gridDim.x; idx = blockIdx.x; }
   else if (mode == 1) { role = 0; nrole = gridDim.x; idx = blockIdx.x; }
   else if (mode == 2) { role = 1; nrole = gridDim.x; idx = blockIdx.x; }
   else { role = blockIdx.x & 1; nrole = gridDim.x / 2; idx = blockIdx.x / 2; }
-  const size_t chunk = 4096;  // float4 per 64 KiB
   const size_t nchunks = n4 / chunk;
   for (size_t c = idx; c < nchunks; c += nrole) {
     const size_t base = c * chunk;
@@ -57,12 +65,13 @@ __global__ void __launch_bounds__(512) mix(const float4* __restrict__ in, float4
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         const size_t j = i + u * 512;
-        v[u] = role == 1 ? ld_cg(ws + wbase + j) : ld_cs(in + base + j);
+        v[u] = role == 1 ? ld_cg(ws + wbase + j) : (pol ? ld_df(in + base + j) : ld_cs(in + base + j));
       }
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         const size_t j = i + u * 512;
         if (role == 0) st_cg(ws + wbase + j, v[u]);
+        else if (pol) st_df(out + base + j, v[u]);
         else st_cs(out + base + j, v[u]);
       }
     }
@@ -73,7 +82,10 @@ int main(int argc, char** argv) {
   const size_t N = (size_t)8 << 30;  // bytes per HBM stream per launch (in and out buffers)
   // workspace footprint in MiB (default 64 = one cfg5 row; 37 ~ K6's per-CTA rows for cfg4)
   const size_t WS = (size_t)(argc > 1 ? atoi(argv[1]) : 64) << 20;
-  printf("workspace footprint %zu MiB\n", WS >> 20);
+  const int pol = argc > 2 ? atoi(argv[2]) : 0;            // 0: .cs streams, 1: default-policy streams
+  // KiB per chunk -> float4 count (multiples of 64 KiB: one pass of 512 threads x UNROLL vectors)
+  const size_t chunk = (size_t)((argc > 3 ? atoi(argv[3]) : 64) / 64 * 64 > 0 ? (argc > 3 ? atoi(argv[3]) : 64) / 64 * 64 : 64) << 6;
+  printf("workspace footprint %zu MiB, stream policy %s, chunk %zu KiB\n", WS >> 20, pol ? "default" : ".cs", chunk >> 6);
   char *in, *out, *ws;
   cudaMalloc(&in, N);
   cudaMalloc(&out, N);
@@ -85,12 +97,12 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const char* names[] = {"copy (in+out)", "A only (in+wsW)", "B only (wsR+out)", "mix (in+wsW | wsR+out)"};
-  for (int occ : {1, 2}) {
+  for (int occ : {2, 4}) {
     for (int mode = 0; mode < 4; ++mode) {
       float best = 1e30f;
       for (int t = 0; t < 4; ++t) {
         cudaEventRecord(e0);
-        mix<<<148 * occ, 512>>>((const float4*)in, (float4*)out, (float4*)ws, N / 16, WS / 16, mode);
+        mix<<<148 * occ, 512>>>((const float4*)in, (float4*)out, (float4*)ws, N / 16, WS / 16, mode, pol, chunk);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;

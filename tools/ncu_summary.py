@@ -17,6 +17,14 @@ KEYS = [
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
     "smsp__inst_executed.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    # memory-system view (round 2, session 4): LSU data pipe, SM -> XBAR write port, L2 slices, cross-die sectors
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__m_l1tex2xbar_write_bytes.sum.pct_of_peak_sustained_elapsed", "l1tex__m_l1tex2xbar_write_bytes.sum.per_second",
+    "l1tex__m_xbar2l1tex_read_bytes.sum.per_second", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_sectors.sum.per_second", "lts__t_sectors_srcunit_tex.sum.per_second",
+    "lts__t_sectors_srcunit_ltcfabric.sum.per_second", "lts__t_sector_hit_rate.pct",
+    "dram__bytes.sum.per_second",
 ]
 
 
