@@ -81,6 +81,16 @@
 // Workspace cache hints: bit 0 = A's workspace stores carry an L2 evict_last
 // policy, bit 1 = B's workspace loads carry evict_first (the data is dead once
 // read).
+// Which tile (A: input tile a = j14..23; B: workspace tile v) the CTA's i-th
+// item c + i G names: a fixed bit permutation of that number, the same for A
+// and B (so A(r+1, .) still overwrites exactly what B(r, .) read).  0: identity
+// (CTAs c, c+1 share every 128-byte workspace line); 1: the low item bits are
+// the tile bits that sit lowest in the OUTPUT position (out bits 10..16), so
+// the 148 CTAs write neighbouring 4 KiB runs at any moment; 2: bit 0 kept, bits
+// 1..4 -> out bits 10..13.
+#ifndef CHW_SWEEP_TPERM
+#define CHW_SWEEP_TPERM 0
+#endif
 #ifndef CHW_SWEEP_WSHINT
 #define CHW_SWEEP_WSHINT 0
 #endif
@@ -248,6 +258,16 @@ __device__ __forceinline__ void trace_stamp(uint32_t cta, uint32_t grp, uint32_t
   } while (0)
 #endif
 
+__device__ __forceinline__ uint32_t tile_of(uint32_t item) {
+#if CHW_SWEEP_TPERM == 1
+  return deposit<BL<9, 8, 7, 6, 4, 3, 2, 5, 1, 0>>(item);
+#elif CHW_SWEEP_TPERM == 2
+  return deposit<BL<0, 9, 8, 7, 6, 4, 3, 2, 5, 1>>(item);
+#else
+  return item;
+#endif
+}
+
 template <bool SCALE, bool SEQ = false>
 __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
     sweep_m24_kernel(const float* __restrict__ in, float* __restrict__ out, float* __restrict__ ws,
@@ -285,7 +305,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       const uint32_t r = u / nt, i = u - r * nt;
       const int st = (int)(u % SA);
       mbar_expect_tx_cta(&fullA[st], TB);
-      const uint64_t a = c + (uint64_t)i * G;
+      const uint64_t a = (uint64_t)tile_of(c + i * G);
       bulk_g2s(ringA + st * TILE, in + ((uint64_t)r << 24) + (a << 14), TB, &fullA[st], pol);
     };
     if (gt == 0) {
@@ -322,7 +342,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bar();
       if (gt == 0) {
-        const uint32_t a = c + i * G;
+        const uint32_t a = tile_of(c + i * G);
         if (r & 1u)
           tensor4_s2g(&tmapP, stage, 0, (int)a, 0, 0);  // layout Q: 1024 runs of 64 B
         else
@@ -347,7 +367,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       SWEEP_STAMP(0, 2);
       if (CHW_SWEEP_ONLY != 1 && r >= 1) mbar_wait_cta(&regionfree[i], (r - 1) & 1u);  // B(r-1, a) has been read
       SWEEP_STAMP(0, 3);
-      const uint32_t a = c + i * G;
+      const uint32_t a = tile_of(c + i * G);
       if (r & 1u)
         store_global<P::AL1, P::AOutQ, false, (CHW_SWEEP_WSHINT & 1) ? Cache::kL2Last : Cache::kL2>(
             ws + ((uint64_t)a << 4), v, gtv, 1.0f);
@@ -390,7 +410,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
           (void)ld_acquire_gpu_u32(&cnt[r]);  // synchronizes with every A tile's release
         }
       }
-      const uint32_t t = c + i * G;
+      const uint32_t t = tile_of(c + i * G);
       if (r & 1u)
         load_global<P::BL0, IdMap, Cache::kL2>(ws + ((uint64_t)t << 14), v, gtv);
       else
@@ -408,7 +428,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       SWEEP_STAMP(1, 1);
       butterflies<P::BL0, P::BB0, false>(v);  // every loaded value consumed
       SWEEP_STAMP(1, 2);
-      const uint32_t t = c + i * G;
+      const uint32_t t = tile_of(c + i * G);
       float* orow = out + ((uint64_t)r << 24);
       const uint32_t outer = deposit<P::BOuter>(t);
       using MapO = typename std::conditional<SEQ, SeqMap<P::BOutH, 24>, P::BOutH>::type;
@@ -449,7 +469,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       mbar_expect_tx_cta(fullBp, TB);
-      const uint32_t t = c + i * G;
+      const uint32_t t = tile_of(c + i * G);
       if (r & 1u)
         bulk_g2s(stageB, ws + ((uint64_t)t << 14), TB, fullBp, pol);
       else
@@ -479,7 +499,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       // A(r+1, t) rewrites them — before `regionfree` lets A write there.
       // (Layout-P tiles share every 128-byte line with another CTA's tile.)
       if (r & 1u) {
-        const float* reg = ws + ((uint64_t)(c + i * G) << 14);
+        const float* reg = ws + ((uint64_t)tile_of(c + i * G) << 14);
 #pragma unroll
         for (int q = 0; q < 4; ++q) discard_l2_128(reg + (gt + q * NT) * 32u);
       }
@@ -503,7 +523,7 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       // L0 -> L1 through the 32 KiB buffer one t0-half at a time; B1 (which
       // never touches t0) and the stores run per half, so only 64 extra
       // registers are live.
-      const uint32_t t = c + i * G;
+      const uint32_t t = tile_of(c + i * G);
       float* orow = out + ((uint64_t)r << 24);
       const uint32_t outer = deposit<P::BOuter>(t);
       using MapO = typename std::conditional<SEQ, SeqMap<P::BOutH, 24>, P::BOutH>::type;

@@ -68,3 +68,30 @@ def test_k9b_layouts_conflict_free():
     b2 = Layout([12, 11, 0, 1, 3, 4], [10, 9, 8, 7, 2, 5, 6])
     s2 = [(7, 2), (10, 2), (8, 3), (9, 4)]
     assert _ideal(smem_cost(b1, s2, 4, 2)) and _ideal(smem_cost(b2, s2, 4, 2))
+
+
+def test_k10_cluster_plan():
+    """K10 (csrc/clusterm16.cuh: ClusterF32M16): the in-quarter transpose, the
+    exchange blocks (writer side per destination, reader side) and the output
+    stores are conflict-free / whole sectors, and the three layouts cover all
+    16 row bits exactly once."""
+    l0 = Layout([0, 1, 9, 10, 11, 12], [2, 3, 4, 5, 6, 7, 8, 13])
+    l1 = Layout([2, 3, 4, 5, 6, 13], [7, 8, 9, 0, 1, 10, 11, 12])
+    s1 = [(7, 2), (8, 3), (9, 4)]
+    assert _ideal(smem_cost(l0, [], 4, 2, 8))    # stage read (natural order)
+    assert _ideal(smem_cost(l0, s1, 4, 2, 8))    # transpose store
+    assert _ideal(smem_cost(l1, s1, 4, 2, 8))    # transpose load (scalar)
+    lw = Layout([0, 1, 9, 10, 11, 8], [2, 3, 4, 5, 6, 7])
+    lr = Layout([13, 12, 2, 3, 0, 1], [4, 5, 6, 7, 8, 9, 10, 11])
+    sx = [(5, 2), (6, 3)]
+    assert _ideal(smem_cost(lw, sx, 4, 2, 2))    # exchange block store
+    assert _ideal(smem_cost(lr, sx, 4, 2, 8))    # exchange read
+    out = [13, 12, 8, 7, 6, 5, 4, 3, 2, 11, 10, 9, 1, 0]
+    g = global_cost(lr, lambda b: out[b], 4, 2, 8)
+    assert g["vec_bytes"] == 16 and g["partial_sectors_per_instr"] == 0 and g["sectors_per_instr"] == 16
+    # exchange-tile bit e_k -> row bit j
+    e_to_j = [2, 3, 7, 8, 9, 10, 11, 12, 13, 4, 5, 6, 14, 15]
+    bits = [0, 1, 9, 10, 11, 12] + [2, 3, 4, 5, 6, 13] + [e_to_j[e] for e in (13, 12, 2, 3)]
+    assert sorted(bits) == list(range(16))
+    # the dyadic position of row bit j is 15 - j; the CTA rank supplies j0, j1
+    assert [15 - e_to_j[e] for e in range(14)] == out
