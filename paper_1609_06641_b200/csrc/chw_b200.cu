@@ -229,11 +229,12 @@ bool order_fused(chw_dtype dtype, int m, chw_order order) {
   if (order == CHW_ORDER_DYADIC) return true;
   if (m <= k1max_of(dtype)) return true;
   // sequency is an XOR-linear map of the dyadic position: folded into the
-  // f32 long-row kernels' stores (K6 m = 16, K9 m = 24); natural at m = 16
-  // (K6's second phase carries j0..j3, so its natural-order runs stay whole)
+  // f32 long-row kernels' stores (K6 m = 16, K9 m = 24); natural order needs
+  // the second phase to carry j0..j3 so its runs stay whole 64-byte pieces:
+  // K6 at m = 16, the K9n plan at m = 24
   if (dtype != CHW_F32) return false;
   if (order == CHW_ORDER_SEQUENCY) return m == 16 || m == 24;
-  return order == CHW_ORDER_NATURAL && m == 16;
+  return order == CHW_ORDER_NATURAL && (m == 16 || m == 24);
 }
 
 size_t ordered_workspace(chw_dtype dtype, int64_t batch, int m, chw_order order) {
@@ -298,14 +299,15 @@ chw_status forward_impl(const void* in, void* out, chw_dtype dtype, int64_t batc
   // store map (identity / inverse Gray code), zero extra bytes.
   if (m <= k1max_of(dtype))
     return ordered_k1_impl(in, out, dtype, batch, m, mode, order == CHW_ORDER_SEQUENCY, st);
-  if (order_fused(dtype, m, order)) {  // f32 sequency at m = 16 / 24, natural at m = 16
+  if (order_fused(dtype, m, order)) {  // f32 natural / sequency at m = 16 (K6) and m = 24 (K9n / K9)
     const bool ortho = (mode == CHW_ORTHONORMAL);
     const float sc = (float)ortho_scale(m);
     auto* i = static_cast<const float*>(in);
     auto* o = static_cast<float*>(out);
     if (m == 16)
       return launch_rowpipe_m16_ordered(order == CHW_ORDER_NATURAL ? 1 : 2, ortho, i, o, ws, batch, sc, st);
-    return launch_sweep_m24(ortho, i, o, ws, batch, sc, st, true);
+    // (the sweep also serves the fused orders when CHW_B200_M24=t selects K4T for the dyadic order)
+    return launch_sweep_m24(ortho, i, o, ws, batch, sc, st, order == CHW_ORDER_NATURAL ? 1 : 2);
   }
   // Other orders: dyadic result into the workspace, then one coalesced gather.
   void* tmp = static_cast<char*>(ws) + align256(workspace_for(dtype, batch, m));

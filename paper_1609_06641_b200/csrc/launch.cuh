@@ -452,9 +452,10 @@ inline char m24_mode() {
 inline size_t sweep_m24_workspace(int64_t batch) {
   return ((size_t)64 << 20) + (((size_t)std::max<int64_t>(batch, 0) * 4 + 255) & ~(size_t)255);
 }
-// K9 launcher (sweep.cu, its own translation unit); seq: sequency output order.
+// K9 launcher (sweep.cu, its own translation unit); order: 0 dyadic, 1 natural
+// (K9n), 2 sequency — all folded into the sweep's stores.
 chw_status launch_sweep_m24(bool scale_mode, const float* in, float* out, void* ws, int64_t batch, float scale,
-                            cudaStream_t st, bool seq = false);
+                            cudaStream_t st, int order = 0);
 // Natural (order 1) / sequency (order 2) folded into the f32 m = 16 (K6,
 // inst_f32_m16.cu) store map.
 chw_status launch_rowpipe_m16_ordered(int order, bool scale_mode, const float* in, float* out, void* ws,
@@ -524,7 +525,9 @@ size_t k4_workspace_m(int m, int64_t batch, size_t inter) {
     if constexpr (std::is_same<T, float>::value && MLO == 16) return rowpipe_workspace(batch);
     if constexpr (std::is_same<T, float>::value && MLO == 24) {
       if (m24_mode() == 's') return sweep_m24_workspace(batch);  // K9: one L2-resident row
-      return (size_t)std::min<int64_t>(batch, kM24Chunk) << 26;  // K4T: 16-row intermediate
+      // K4T: 16-row intermediate (never less than the sweep needs: the fused
+      // natural / sequency orders run on the sweep in either mode)
+      return std::max((size_t)std::min<int64_t>(batch, kM24Chunk) << 26, sweep_m24_workspace(batch));
     }
     return (size_t)batch * ((size_t)1 << m) * inter;
   }

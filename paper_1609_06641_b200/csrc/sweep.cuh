@@ -143,7 +143,45 @@ struct SweepF32M24 {
   using BOut = ListMap<21, 20, 18, 17, 9, 8, 7, 6, 5, 4, 3, 2, 1, 0>;
   using BOuter = BL<23, 22, 16, 15, 14, 19, 13, 12, 11, 10>;
   static constexpr int E = AL0::E;
+  static constexpr bool kNatural = false;
   static_assert(AL0::NT == NT && BL0::NT == NT && BL0::E == E, "group shape");
+};
+
+// The same sweep with NATURAL output order (chw_order 1, orderings.hpp:45-78)
+// folded in.  The output position of row bit j is j itself, so the B tile's
+// passengers must be j0..j3 (whole 64-byte runs in the output): workspace addr
+// 0..3 = j0..j3, v bits = j4..j13 in order.  A butterflies j0, j1 (first
+// layout, they are its 16-byte vector) and j4..j13; j0, j1 ride along in its
+// second layout, so both sides of A's transpose are 16-byte accesses.  B
+// butterflies j2, j3 and j14..j23: its first layout holds t0..t3 in registers,
+// which is conflict-free only if the stage is written under TMA's 64-byte
+// swizzle (BStage); no register bit is shared between B's two layouts, so the
+// transpose is in place in the stage (no half buffer) and the stores are
+// scalar, two whole 64-byte runs per warp instruction.
+struct SweepNatF32M24 {
+  static constexpr int M = 24;
+  static constexpr int TILE = 1 << 14;
+  static constexpr int NT = 128;
+  static constexpr uint32_t NTILES = 1024;
+  using AL0 = Layout<BL<0, 1, 5, 6, 7, 8, 9>, BL<2, 3, 4, 10, 11, 12, 13>>;
+  using AL1 = Layout<BL<0, 1, 4, 10, 11, 12, 13>, BL<2, 3, 5, 6, 7, 8, 9>>;
+  using AS = Swz<5, 4>;
+  using AB0 = BL<0, 1, 5, 6, 7, 8, 9>;
+  using AB1 = BL<4, 10, 11, 12, 13>;
+  using AOutP = IdMap;                                                          // tile base a << 14
+  using AOutQ = ListMap<0, 1, 2, 3, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23>;   // tile base a << 4
+  // B tile bits t0..t3 = j0..j3 (addr 0..3), t4..t13 = j14..j23
+  using BL0 = Layout<BL<0, 1, 2, 3, 7, 8, 9>, BL<4, 5, 6, 10, 11, 12, 13>>;
+  using BL1 = Layout<BL<4, 5, 6, 10, 11, 12, 13>, BL<0, 1, 2, 3, 7, 8, 9>>;
+  using BStage = Swz<5, 2, 6, 3>;        // CU_TENSOR_MAP_SWIZZLE_64B in float-index bits
+  using BS = Swz<5, 2, 6, 3, 7, 4>;
+  using BB0 = BL<2, 3, 7, 8, 9>;
+  using BB1 = BL<4, 5, 6, 10, 11, 12, 13>;
+  using BInP = ListMap<0, 1, 2, 3, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23>;
+  using BOut = ListMap<0, 1, 2, 3, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23>;    // natural position; tile index v -> v << 4
+  static constexpr int E = AL0::E;
+  static constexpr bool kNatural = true;
+  static_assert(AL0::NT == NT && AL1::NT == NT && BL0::NT == NT && BL1::NT == NT && BL0::E == E, "group shape");
 };
 
 // B-side tensor map (layout P rows): the workspace as [4][256][1024][16]
@@ -543,6 +581,139 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       SWEEP_STAMP(1, 3);
     }
 #endif
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K9n: the K9 sweep with NATURAL output order folded in (plan SweepNatF32M24).
+// Same roles, mbarriers and row protocol as sweep_m24_kernel; the B group
+// transposes in place in its stage (shared memory: two A stages + one B
+// stage), loads both workspace layouts through swizzling tensor maps and
+// stores scalars in whole 64-byte runs.
+// ---------------------------------------------------------------------------
+template <bool SCALE>
+__global__ void __launch_bounds__(2 * SweepNatF32M24::NT, 1)
+    sweep_nat_m24_kernel(const float* __restrict__ in, float* __restrict__ out, float* __restrict__ ws,
+                         uint32_t* __restrict__ cnt, uint32_t rows, float scale,
+                         const __grid_constant__ TmapParam tmapP, const __grid_constant__ TmapParam tmapQ) {
+  using P = SweepNatF32M24;
+  constexpr int TILE = P::TILE;
+  constexpr uint32_t TB = TILE * 4;
+  constexpr int NT = P::NT;
+  constexpr int SA = 2;
+  constexpr int MAXT = 8;
+  extern __shared__ __align__(1024) float smem_sn[];
+  float* ringA = smem_sn;
+  float* stageB = smem_sn + SA * TILE;
+  __shared__ __align__(8) uint64_t fullA[SA], fullB, regionfree[MAXT];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t G = gridDim.x, c = blockIdx.x;
+  const uint32_t nt = (P::NTILES - c + G - 1) / G;  // tiles this CTA owns: c, c+G, ...
+  if (nt == 0 || nt > MAXT) return;
+  if (tid == 0) {
+    for (int s = 0; s < SA; ++s) mbar_init_cta(&fullA[s], 1);
+    mbar_init_cta(&fullB, 1);
+    for (int k = 0; k < MAXT; ++k) mbar_init_cta(&regionfree[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t total = rows * nt;
+  float v[P::E];
+  if (tid < (uint32_t)NT) {  // ---- A group
+    const uint32_t gt = tid;
+    auto bar = [] { named_bar(1, NT); };
+    uint64_t pol = 0;
+    auto issue = [&](uint32_t u) {
+      const uint32_t r = u / nt, i = u - r * nt;
+      const int st = (int)(u % SA);
+      mbar_expect_tx_cta(&fullA[st], TB);
+      const uint64_t a = c + (uint64_t)i * G;
+      bulk_g2s(ringA + st * TILE, in + ((uint64_t)r << 24) + (a << 14), TB, &fullA[st], pol);
+    };
+    if (gt == 0) {
+      pol = l2_evict_first_policy();
+      for (uint32_t u = 0; u < (uint32_t)SA && u < total; ++u) issue(u);
+    }
+    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
+      const int st = (int)(u % SA);
+      float* stage = ringA + st * TILE;
+      uint32_t gtv = gt;  // opaque thread index (see sweep_m24_kernel)
+      asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
+      mbar_wait_cta(&fullA[st], (u / SA) & 1u);
+      smem_load<P::AL0, NoSwz>(stage, v, gtv);
+      butterflies<P::AL0, P::AB0, false>(v);
+      bar();
+      smem_store<P::AL0, P::AS>(stage, v, gtv);
+      bar();
+      smem_load<P::AL1, P::AS>(stage, v, gtv);
+      bar();  // every thread has read the stage: refill it
+      if (gt == 0 && u + SA < total) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(u + SA);
+      }
+      butterflies<P::AL1, P::AB1, false>(v);
+      if (r >= 1) mbar_wait_cta(&regionfree[i], (r - 1) & 1u);  // B(r-1, a) has been read
+      const uint32_t a = c + i * G;
+      if (r & 1u)
+        store_global<P::AL1, P::AOutQ, false, Cache::kL2>(ws + ((uint64_t)a << 4), v, gtv, 1.0f);
+      else
+        store_global<P::AL1, P::AOutP, false, Cache::kL2>(ws + ((uint64_t)a << 14), v, gtv, 1.0f);
+      if (i + 1 == nt) {  // this CTA's last A tile of row r: publish all nt of them
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        bar();
+        if (gt == 0) red_release_add(&cnt[r], nt);
+      }
+    }
+  } else {  // ---- B group
+    const uint32_t gt = tid - NT;
+    auto bar = [] { named_bar(2, NT); };
+    uint64_t pol = 0;
+    auto issue = [&](uint32_t u, bool wait) -> bool {
+      const uint32_t r = u / nt, i = u - r * nt;
+      if (i == 0) {
+        if (ld_relaxed_u32(&cnt[r]) < P::NTILES) {
+          if (!wait) return false;
+          while (ld_relaxed_u32(&cnt[r]) < P::NTILES) __nanosleep(64);
+        }
+        (void)ld_acquire_gpu_u32(&cnt[r]);  // synchronizes with every A tile's release
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      mbar_expect_tx_cta(&fullB, TB);
+      const uint32_t t = c + i * G;
+      // both layouts through 64-byte-swizzling tensor maps (Q: the contiguous region as [4][256][16])
+      if (r & 1u)
+        tensor3_g2s(stageB, &tmapQ, 0, 0, (int)(4u * t), &fullB);
+      else
+        tensor4_g2s_hint(stageB, &tmapP, 0, (int)t, 0, 0, &fullB, pol);
+      return true;
+    };
+    bool pending = false;
+    if (gt == 0) {
+      pol = l2_evict_normal_policy();
+      pending = total > 0;
+    }
+    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
+      if (pending) pending = !issue(u, true);
+      uint32_t gtv = gt;
+      asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
+      mbar_wait_cta(&fullB, u & 1u);
+      // B(r, t)'s workspace bytes are in shared memory: A(r+1, t) may overwrite them.
+      if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
+      smem_load<P::BL0, P::BStage>(stageB, v, gtv);
+      butterflies<P::BL0, P::BB0, false>(v);
+      bar();  // every thread has read the stage (TMA's swizzle): rewrite it
+      smem_store<P::BL0, P::BS>(stageB, v, gtv);
+      bar();
+      smem_load<P::BL1, P::BS>(stageB, v, gtv);
+      bar();  // the stage is free: load the next B tile
+      if (gt == 0 && u + 1 < total) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        pending = !issue(u + 1, false);
+      }
+      butterflies<P::BL1, P::BB1, false>(v);
+      const uint32_t t = c + i * G;  // v bits = j4..j13 in order: natural position t << 4
+      store_global<P::BL1, P::BOut, SCALE, Cache::kStream>(out + ((uint64_t)r << 24), v, gtv, scale, t << 4);
+    }
   }
 }
 

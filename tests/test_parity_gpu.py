@@ -489,6 +489,49 @@ def test_natural_fused_f32_m16(cuda, rows):
     assert _rel_l2(got, want) <= F32_TOL
 
 
+@pytest.mark.parametrize("rows", [1, 3])
+def test_natural_fused_f32_m24(cuda, rows):
+    """f2: natural order folded into the m = 24 row sweep (K9n: the second
+    phase carries j0..j3, in-place tile transposes, swizzling tensor maps) —
+    bit-exact integer probe against the dyadic result permuted by bit
+    reversal (orderings.hpp:45-78), in place and out of place, one launch, no
+    gather workspace; orthonormal f32 within tolerance of the reference's
+    natural FWHT."""
+    import torch
+
+    chw = _chw()
+    m = 24
+    rng = np.random.default_rng(2400 + rows)
+    xi = rng.integers(-3, 4, size=(rows, 1 << m), dtype=np.int64)
+    dy = oracle.chw_batch(xi, U)
+    idx = np.arange(1 << m, dtype=np.int64)
+    rev = np.zeros_like(idx)
+    for b in range(m):
+        rev |= ((idx >> b) & 1) << (m - 1 - b)
+    ref = dy[:, rev]
+    t = torch.from_numpy(xi).to(cuda).to(torch.float32)
+    out = torch.empty_like(t)
+    n_dy = chw.launch_count()
+    chw.chw_forward_batched_(t.clone(), chw.ScalingMode.Unnormalized)
+    n_dy = chw.launch_count() - n_dy
+    n_nat = chw.launch_count()
+    chw.chw_forward_batched_(t, chw.ScalingMode.Unnormalized, out=out, order=chw.ORDER_NATURAL)
+    n_nat = chw.launch_count() - n_nat
+    chw.chw_forward_batched_(t, chw.ScalingMode.Unnormalized, order=chw.ORDER_NATURAL)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.to(torch.float64).cpu().numpy().astype(np.int64), ref)
+    assert np.array_equal(t.to(torch.float64).cpu().numpy().astype(np.int64), ref)
+    assert n_nat == n_dy, "natural order must not add a gather pass"
+    assert chw.workspace_bytes_ordered(chw.DTYPE_F32, rows, 1 << m, chw.ORDER_NATURAL) == \
+        chw.workspace_bytes(chw.DTYPE_F32, rows, 1 << m)
+    x = rng.standard_normal(size=(1, 1 << m)).astype(np.float32)
+    tx = torch.from_numpy(x).to(cuda)
+    chw.chw_forward_batched_(tx, chw.ScalingMode.Orthonormal, order=chw.ORDER_NATURAL)
+    got = tx.cpu().numpy().astype(np.float64)
+    want = oracle.simple("fwht_natural", x[0].astype(np.float64), O)[None, :]
+    assert _rel_l2(got, want) <= F32_TOL
+
+
 @pytest.mark.parametrize("dt", ["f32", "bf16", "i64"])
 @pytest.mark.parametrize("m", [3, 10, 12, 16])
 def test_orders_other_dtypes(cuda, dt, m):
