@@ -70,6 +70,9 @@ size_t haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
 size_t haar_inverse_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
 chw_status haar_inverse_device(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
                                chw_mode mode, void* ws, cudaStream_t st);
+int haar_walsh_prefix_bits(chw_dtype dtype, int m);
+chw_status haar_walsh_prefix_device(void* x, chw_dtype dtype, int64_t batch, uint64_t n, int K, chw_mode mode,
+                                    cudaStream_t st);
 chw_status haar_forward_device(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,
                                chw_mode mode, void* ws, cudaStream_t st);
 }  // namespace chwb
@@ -640,18 +643,23 @@ chw_status chw_b200_haar_walsh_forward(const void* in, void* out, chw_dtype dtyp
   if (in != out) CHW_CUDA(cudaMemcpyAsync(out, in, (size_t)batch * n * es, cudaMemcpyDeviceToDevice, st));
   const int m = level_of(n);
   if (m < 2) return CHW_OK;
-  // Gather block j of every row into a contiguous [batch][2^j] buffer, run the
-  // batched dyadic kernel on it, scatter back.
+  // Blocks j < K of every row: one shared-memory kernel (haar.cu), one HBM
+  // read and write of the prefix.
+  const int K = haar_walsh_prefix_bits(dtype, m);
+  if (chw_status s = haar_walsh_prefix_device(out, dtype, batch, n, K, mode, st)) return s;
+  if (K >= m) return CHW_OK;
+  // Longer blocks j = K..m-1: gather block j of every row into a contiguous
+  // [batch][2^j] buffer, run the batched dyadic kernel on it, scatter back.
   const size_t tmp_bytes = (size_t)batch * (n / 2) * es;
   size_t inner = 0;
-  for (int j = 1; j <= m - 1; ++j) inner = std::max(inner, workspace_for(dtype, batch, j));
+  for (int j = K; j <= m - 1; ++j) inner = std::max(inner, workspace_for(dtype, batch, j));
   WsLease lease;
   if (chw_status s = lease_workspace("haar_walsh_forward", align256(tmp_bytes) + inner, nullptr, 0, st, &lease))
     return s;
   char* tmp = static_cast<char*>(lease.p);
   void* inner_ws = tmp + align256(tmp_bytes);
   char* o = static_cast<char*>(out);
-  for (int j = 1; j <= m - 1; ++j) {
+  for (int j = K; j <= m - 1; ++j) {
     const size_t blk = ((size_t)1 << j) * es;
     CHW_CUDA(cudaMemcpy2DAsync(tmp, blk, o + blk, n * es, blk, (size_t)batch, cudaMemcpyDeviceToDevice, st));
     if (chw_status s = dyadic_impl(tmp, tmp, dtype, batch, j, mode, inner_ws, st)) return s;

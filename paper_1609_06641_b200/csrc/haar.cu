@@ -314,6 +314,74 @@ chw_status haar_impl(const T* in, T* out, int64_t batch, uint64_t n, bool ortho,
   return CHW_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Haar-Walsh map (transforms.hpp:187-198): a dyadic WHT of every scale block
+// [2^j, 2^(j+1)), j = 1..m-1.  The blocks below 2^K of a row (K <= 13 or 14,
+// whatever fits 64 KiB of shared memory) are done by ONE kernel, one CTA per
+// row: level t = 0..K-2 combines (i, i | 2^t) for every i >= 2^(t+1) with bit
+// t clear — block j takes part in levels t < j, the reference's level order —
+// with the reference's per-butterfly scaling, and the store applies each
+// block's own bit reversal.  One HBM read and write of the prefix instead of a
+// gather, a transform and a scatter per block.
+// ---------------------------------------------------------------------------
+template <class T>
+struct HwIo {
+  using C = T;
+  __device__ static C ld(const T* p) { return *p; }
+  __device__ static void st(T* p, C v) { *p = v; }
+};
+template <>
+struct HwIo<__nv_bfloat16> {
+  using C = float;
+  __device__ static float ld(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+  __device__ static void st(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+};
+
+template <class T>
+__global__ void haar_walsh_smem_kernel(T* __restrict__ x, int64_t stride, uint32_t K, bool ortho) {
+  using C = typename HwIo<T>::C;
+  extern __shared__ __align__(16) unsigned char hw_smem[];
+  C* s = reinterpret_cast<C*>(hw_smem);
+  T* row = x + (int64_t)blockIdx.x * stride;
+  const uint32_t n0 = 1u << K;
+  for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) s[i] = HwIo<T>::ld(row + i);
+  __syncthreads();
+  for (uint32_t t = 0; t + 1 < K; ++t) {
+    for (uint32_t p = threadIdx.x; p < n0 / 2; p += blockDim.x) {
+      const uint32_t i = ((p >> t) << (t + 1)) | (p & ((1u << t) - 1u));
+      if (i >= (2u << t)) {
+        C a, b;
+        HaarOps<C>::bf(s[i], s[i | (1u << t)], ortho, a, b);
+        s[i] = a;
+        s[i | (1u << t)] = b;
+      }
+    }
+    __syncthreads();
+  }
+  for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) {
+    uint32_t src = i;
+    if (i >= 4) {  // blocks 0, 1 (one element) and j = 1 (two elements) are their own reversal
+      const uint32_t j = 31u - (uint32_t)__clz((int)i);
+      src = (1u << j) | (__brev(i - (1u << j)) >> (32u - j));
+    }
+    HwIo<T>::st(row + i, s[src]);
+  }
+}
+
+template <class T>
+chw_status haar_walsh_prefix_impl(T* x, int64_t batch, uint64_t n, int K, bool ortho, cudaStream_t st) {
+  const int smem = (int)(((size_t)1 << K) * sizeof(typename HwIo<T>::C));
+  if (smem > 48 * 1024)
+    CHW_CUDA(cudaFuncSetAttribute(haar_walsh_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int threads = (int)std::min<uint64_t>(512, std::max<uint64_t>(32, ((uint64_t)1 << K) / 2));
+  for (int64_t r0 = 0; r0 < batch; r0 += 0x7fffffff) {
+    const unsigned g = (unsigned)std::min<int64_t>(batch - r0, 0x7fffffff);
+    haar_walsh_smem_kernel<T><<<g, threads, smem, st>>>(x + r0 * (int64_t)n, (int64_t)n, (uint32_t)K, ortho);
+    if (chw_status s = check_launch("haar_walsh_smem_kernel")) return s;
+  }
+  return CHW_OK;
+}
+
 }  // namespace
 
 size_t haar_inverse_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {
@@ -363,6 +431,27 @@ size_t haar_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n) {
   const uint64_t smem_max = kSmemMaxBytes / (2 * es);
   if (n <= smem_max || batch <= 0) return 0;
   return 2 * (size_t)batch * (n / 2) * es;
+}
+
+// Largest K such that the blocks below 2^K of a row fit the shared-memory kernel.
+int haar_walsh_prefix_bits(chw_dtype dtype, int m) {
+  const int es = (dtype == CHW_F64 || dtype == CHW_I64) ? 8 : 4;  // bf16 is computed in fp32
+  int kmax = 0;
+  while (((size_t)2 << kmax) * es <= (size_t)kSmemMaxBytes) ++kmax;
+  return std::min(m, kmax);
+}
+
+// In place on x (rows of n): the Haar-Walsh map of the blocks below 2^K.
+chw_status haar_walsh_prefix_device(void* x, chw_dtype dtype, int64_t batch, uint64_t n, int K, chw_mode mode,
+                                    cudaStream_t st) {
+  const bool ortho = (mode == CHW_ORTHONORMAL);
+  switch (dtype) {
+    case CHW_F64: return haar_walsh_prefix_impl(static_cast<double*>(x), batch, n, K, ortho, st);
+    case CHW_F32: return haar_walsh_prefix_impl(static_cast<float*>(x), batch, n, K, ortho, st);
+    case CHW_I64: return haar_walsh_prefix_impl(static_cast<long long*>(x), batch, n, K, false, st);
+    case CHW_BF16: return haar_walsh_prefix_impl(static_cast<__nv_bfloat16*>(x), batch, n, K, ortho, st);
+  }
+  return fail(CHW_ERR_UNSUPPORTED, "haar_walsh_forward: unsupported dtype");
 }
 
 chw_status haar_forward_device(const void* in, void* out, chw_dtype dtype, int64_t batch, uint64_t n,

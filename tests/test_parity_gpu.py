@@ -596,6 +596,20 @@ def test_haar_inverse_structure_error(cuda):
     assert np.max(np.abs(rt - xf)) <= 1e-12
 
 
+@pytest.mark.parametrize("m", [1, 2, 5, 10, 14, 15])
+def test_haar_walsh_f32(cuda, m):
+    """f32 Haar-Walsh map: the one-kernel shared-memory prefix (blocks below
+    2^14) plus the per-block path above it, within the fp32 tolerance of the
+    reference (transforms.hpp:187-198) in both scaling modes."""
+    chw = _chw()
+    rng = np.random.default_rng(1700 + m)
+    x = rng.uniform(-1, 1, size=(3, 1 << m)).astype(np.float32)
+    for mode, om in ((chw.ScalingMode.Orthonormal, O), (chw.ScalingMode.Unnormalized, U)):
+        got = chw.haar_walsh_forward(x, mode).astype(np.float64)
+        ref = np.stack([oracle.simple("haar_walsh_forward", r.astype(np.float64), om) for r in x])
+        assert _rel_l2(got, ref) <= F32_TOL
+
+
 @pytest.mark.parametrize("m", list(range(0, 17)))
 def test_haar_walsh(cuda, golden, m):
     chw = _chw()

@@ -9,7 +9,7 @@ import re
 import subprocess
 import sys
 
-KEYS = ["UBLKCP", "UTMALDG", "UTMASTG", "SYNCS", "UTCHMMA", "UTCBAR", "LDTM", "STTM", "FADD2", "FMUL2", "FADD",
+KEYS = ["UBLKCP", "UTMALDG", "UTMASTG", "SYNCS", "UTCHMMA", "UTCBAR", "LDTM", "STTM", "FADD2", "FFMA2", "FMUL2", "FADD",
         "DADD", "DMUL", "SHFL", "LDS", "STS", "LDG", "STG", "BAR", "LDL", "STL"]
 
 
