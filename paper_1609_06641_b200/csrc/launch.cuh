@@ -19,7 +19,6 @@
 #include "pipelined.cuh"
 #include "rowpipe.cuh"
 #include "clusterm16.cuh"
-#include "k1w.cuh"
 #include "k1t.cuh"
 #include "passtma.cuh"
 
@@ -156,7 +155,10 @@ chw_status prep_kernel(int smem) {
 // K1T (k1t.cuh): TMA-fed single-pass kernel for f32 m = 12 (cfg2, default):
 // 8-stage ring, 2 compute groups.  Same-box A/B: 95.3-95.9 %
 // of HBM peak vs 90.7-91.2 % for the cp.async K1P it replaced (removed, with
-// the other measured ring/group variants, in round 2).
+// the other measured ring/group variants, in round 2).  K1W, a warp-per-row
+// variant with all-vector accesses (8 instead of 14 instructions per element),
+// measured the same throughput at higher SM clocks and was removed too
+// (profiles/r02_ab_k1w.txt).
 template <class Item, int TB, int S, int NG, bool SCALE>
 chw_status launch_k1t_x(const typename Item::IO* in, typename Item::IO* out, int64_t tiles, float scale,
                         cudaStream_t st) {
@@ -172,32 +174,8 @@ chw_status launch_k1t_x(const typename Item::IO* in, typename Item::IO* out, int
   k<<<grid, NG * Item::L0::NT + 32, smem, st>>>(in, out, (uint64_t)tiles, scale);
   return check_launch("k1t_kernel");
 }
-// f32 m = 12 schedule: 'w' K1W warp-per-row kernel (k1w.cuh), 't' K1T.
-inline char m12_mode() {
-  static const char mode = [] {
-    const char* e = std::getenv("CHW_B200_M12");
-    return (e && e[0] == 'w') ? 'w' : 't';
-  }();
-  return mode;
-}
-template <bool SCALE>
-chw_status launch_k1w(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
-  using P = WarpRowF32M12;
-  constexpr auto k = k1w_kernel<SCALE>;
-  constexpr int smem = P::S * P::TILE * 4;
-  if (((uintptr_t)in | (uintptr_t)out) & 15u)
-    return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers must be 16-byte aligned");
-  if (chw_status s = prep_kernel<k>(smem)) return s;
-  int dev = 0, sms = 0;
-  if (chw_status s = current_device(&dev)) return s;
-  CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const unsigned grid = (unsigned)std::min<int64_t>(batch, (int64_t)sms);
-  k<<<grid, (P::NW + 1) * 32, smem, st>>>(in, out, (uint64_t)batch, scale);
-  return check_launch("k1w_kernel");
-}
 template <bool SCALE>
 chw_status launch_k1t(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
-  if (m12_mode() == 'w') return launch_k1w<SCALE>(in, out, batch, scale, st);
   return launch_k1t_x<ItemF32M12, 12, 8, 2, SCALE>(in, out, batch, scale, st);
 }
 
@@ -592,7 +570,7 @@ const char* plan_name_m(int m) {
   } else {
     if (m != M) return plan_name_m<T, M + 1>(m);
     if constexpr (M <= Regime<T>::K1MAX) {
-      if constexpr (std::is_same<T, float>::value && M == 12) return m12_mode() == 'w' ? "k1w-warp-row" : "k1t-tma";
+      if constexpr (std::is_same<T, float>::value && M == 12) return "k1t-tma";
       if constexpr (std::is_same<T, __nv_bfloat16>::value && M == 7)
         if (tc_bf16_m7_enabled()) return "k7tc-tcgen05";
       return K1Select<T, M>::kTuned ? "k1-tuned" : "k1-generic";
