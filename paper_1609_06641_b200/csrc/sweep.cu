@@ -106,66 +106,6 @@ chw_status launch_sweep_nat(const float* in, float* out, void* ws, int64_t batch
   CHW_CUDA(cudaLaunchKernelEx(&cfg, k, in, out, w, cnt, (uint32_t)batch, scale, tp, tq));
   return check_launch("sweep_nat_m24_kernel");
 }
-// K9b tensor map (layout P rows): [4][256][2048][8] floats (addr 22..23,
-// 14..21, 3..13, 0..2), box {8, 1, 256, 4} = one 32 KiB B tile in tile order.
-chw_status sweep_b_tmap(float* ws, TmapParam* t) {
-  TmapEncodeFn fn = nullptr;
-  if (chw_status s = tmap_encoder(&fn)) return s;
-  const cuuint64_t dims[4] = {8, 2048, 256, 4};
-  const cuuint64_t strides[3] = {32, (cuuint64_t)1 << 16, (cuuint64_t)1 << 24};
-  const cuuint32_t box[4] = {8, 1, 256, 4};
-  const cuuint32_t e[4] = {1, 1, 1, 1};
-  CUresult r = fn(reinterpret_cast<CUtensorMap*>(t), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ws, dims, strides, box, e,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(CHW_ERR_CUDA, "chw_forward: cuTensorMapEncodeTiled (m = 24 sweep b) failed");
-  return CHW_OK;
-}
-
-template <bool SCALE>
-chw_status launch_sweep_b(const float* in, float* out, void* ws, int64_t batch, float scale, cudaStream_t st) {
-  using P = SweepBF32M24;
-  constexpr auto k = sweep_b_m24_kernel<SCALE>;
-  constexpr int smem = (2 * P::ATILE + 2 * P::BTILE) * 4;
-  if (((uintptr_t)in | (uintptr_t)out | (uintptr_t)ws) & 15u)
-    return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers and workspace must be 16-byte aligned");
-  if (batch > 0x7fffffffLL) return fail(CHW_ERR_UNSUPPORTED, "chw_forward: batch too large for the m = 24 sweep");
-  if (chw_status s = prep_kernel<k>(smem)) return s;
-  int dev = 0, sms = 0;
-  if (chw_status s = current_device(&dev)) return s;
-  CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const unsigned grid = (unsigned)std::min<int>(sms, (int)P::NTILES);
-  if ((P::NTILES + grid - 1) / grid > 8) return fail(CHW_ERR_UNSUPPORTED, "chw_forward: too few SMs for the sweep");
-  float* w = static_cast<float*>(ws);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ((size_t)64 << 20));
-  TmapParam tm;
-  if (chw_status s = sweep_b_tmap(w, &tm)) return s;
-  CHW_CUDA(cudaMemsetAsync(cnt, 0, (size_t)batch * 4, st));
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(P::NTA + 2 * P::NTB);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CHW_CUDA(cudaLaunchKernelEx(&cfg, k, in, out, w, cnt, (uint32_t)batch, scale, tm));
-  return check_launch("sweep_b_m24_kernel");
-}
-
-// CHW_B200_SWEEP=b selects K9b (64-value threads, 16 warps, 3-layout tiles);
-// default K9 (128-value threads, 8 warps).  Same-box A/B: K9 0.526 / 0.526,
-// K9b 0.490 / 0.492 of HBM peak (profiles/r02_ab_k9b.txt): the extra
-// transposes and barriers cost more than the doubled warp count recovers.
-char sweep_variant() {
-  static const char v = [] {
-    const char* e = std::getenv("CHW_B200_SWEEP");
-    return (e && e[0] == 'b') ? 'b' : 'a';
-  }();
-  return v;
-}
 }  // namespace
 
 chw_status launch_sweep_m24(bool scale_mode, const float* in, float* out, void* ws, int64_t batch, float scale,
@@ -176,11 +116,8 @@ chw_status launch_sweep_m24(bool scale_mode, const float* in, float* out, void* 
   if (order == 2)  // sequency
     return scale_mode ? launch_sweep_t<true, true>(in, out, ws, batch, scale, st)
                       : launch_sweep_t<false, true>(in, out, ws, batch, scale, st);
-  if (sweep_variant() == 'a')
-    return scale_mode ? launch_sweep_t<true, false>(in, out, ws, batch, scale, st)
-                      : launch_sweep_t<false, false>(in, out, ws, batch, scale, st);
-  return scale_mode ? launch_sweep_b<true>(in, out, ws, batch, scale, st)
-                    : launch_sweep_b<false>(in, out, ws, batch, scale, st);
+  return scale_mode ? launch_sweep_t<true, false>(in, out, ws, batch, scale, st)
+                    : launch_sweep_t<false, false>(in, out, ws, batch, scale, st);
 }
 
 }  // namespace chwb

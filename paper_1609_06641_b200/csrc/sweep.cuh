@@ -36,61 +36,41 @@
 
 #include "passtma.cuh"
 
+// Compile-time switches.  The defaults are the shipped kernel; the others are
+// the A/B and diagnostic builds behind profiles/r02_ab_sweep_*.txt
+// (tools/build_ab.sh).  Measured slower and removed from the source in round
+// 2: A tiles leaving through a TMA store (0.502 vs 0.535), B tiles loaded
+// straight from L2 into registers (0.464), L2 discard of consumed layout-Q
+// regions (0.522), butterflying the passengers j2, j3 in A instead of B
+// (0.526 vs 0.546), and K9b — 64-value threads, 16 warps, three layouts (0.49).
 #ifndef CHW_SWEEP_OPAQUE
-#define CHW_SWEEP_OPAQUE 1
+#define CHW_SWEEP_OPAQUE 1  // opaque thread index: keeps swizzled addresses out of live registers (no spills)
 #endif
 // Debug builds (-DCHW_SWEEP_TRACE=1, tools/sweep_trace.py) record %globaltimer
 // stamps per tile for CTAs 0 and 1: [cta][group][item][event].
-// Passengers j2, j3 butterflied by B instead of A (A 12 bits, B 12 bits):
-// same-box A/B 0.546 / 0.546 vs 0.526 / 0.526 (profiles/r02_ab_sweep_rebal.txt).
-#ifndef CHW_SWEEP_REBAL
-#define CHW_SWEEP_REBAL 1
-#endif
-// A tiles leave through shared memory and a TMA store (bulk for layout P,
-// tensor box for layout Q) instead of 32 STG.128 per thread.  Measured slower
-// (0.502 vs 0.535: the stage is held until the store has read it and two more
-// shared-memory passes per tile), so off (profiles/r02_ab_sweep_atma.txt).
-#ifndef CHW_SWEEP_ATMA
-#define CHW_SWEEP_ATMA 0
-#endif
-// B tiles come straight from L2 into registers (16-byte .cg loads, the next
-// tile prefetched into the freed registers halfway through the current one)
-// instead of a TMA copy + shared-memory read: two fewer shared-memory passes
-// per tile pair, and the freed 64 KiB stage becomes a third A stage.
-// Measured slower (0.464 vs 0.534, at 1965 MHz without power capping: the L2
-// latency is exposed and the extra live registers spill), so off
-// (profiles/r02_ab_sweep_bldg.txt).
-#ifndef CHW_SWEEP_BLDG
-#define CHW_SWEEP_BLDG 0
-#endif
-// Drop the dead L2 lines of consumed layout-Q B regions (discard.global.L2)
-// before A rewrites them.  Measured slower (0.522 vs 0.535,
-// profiles/r02_ab_sweep_discard.txt), so off.
-#ifndef CHW_SWEEP_DISCARD
-#define CHW_SWEEP_DISCARD 0
-#endif
 #ifndef CHW_SWEEP_TRACE
 #define CHW_SWEEP_TRACE 0
 #endif
 // Diagnostic builds only (wrong results): 1 = the A group alone (no waits on B),
-// 2 = the B group alone (no waits on A) — each group's stand-alone tile rate
-// (profiles/r02_ab_sweep_only.txt).
+// 2 = the B group alone (no waits on A), 3 = both warp groups run B tiles —
+// each group's stand-alone tile rate (profiles/r02_ab_sweep_only.txt).
 #ifndef CHW_SWEEP_ONLY
 #define CHW_SWEEP_ONLY 0
 #endif
-// Workspace cache hints: bit 0 = A's workspace stores carry an L2 evict_last
-// policy, bit 1 = B's workspace loads carry evict_first (the data is dead once
-// read).
 // Which tile (A: input tile a = j14..23; B: workspace tile v) the CTA's i-th
 // item c + i G names: a fixed bit permutation of that number, the same for A
 // and B (so A(r+1, .) still overwrites exactly what B(r, .) read).  0: identity
 // (CTAs c, c+1 share every 128-byte workspace line); 1: the low item bits are
 // the tile bits that sit lowest in the OUTPUT position (out bits 10..16), so
 // the 148 CTAs write neighbouring 4 KiB runs at any moment; 2: bit 0 kept, bits
-// 1..4 -> out bits 10..13.
+// 1..4 -> out bits 10..13.  Measured 0.527 / 0.516 / 0.521
+// (profiles/r02_ab_sweep_tperm.txt).
 #ifndef CHW_SWEEP_TPERM
 #define CHW_SWEEP_TPERM 0
 #endif
+// Workspace cache hints: bit 0 = A's workspace stores carry an L2 evict_last
+// policy, bit 1 = B's workspace loads carry evict_first (the data is dead once
+// read).  Measured 0.506 / 0.526 / 0.515 vs 0.526 (profiles/r02_ab_sweep_wshint.txt).
 #ifndef CHW_SWEEP_WSHINT
 #define CHW_SWEEP_WSHINT 0
 #endif
@@ -107,12 +87,8 @@ struct SweepF32M24 {
   using AL1 = Layout<BL<2, 3, 4, 10, 11, 12, 13>, BL<5, 6, 0, 1, 7, 8, 9>>;
   using AS = Swz<5, 2, 6, 3, 7, 4>;
   using AB0 = BL<0, 1, 5, 6, 7, 8, 9>;
-#if CHW_SWEEP_REBAL
   // passengers j2, j3 are butterflied by B (register bits t0, t1 of BL0)
   using AB1 = BL<4, 10, 11, 12, 13>;
-#else
-  using AB1 = BL<2, 3, 4, 10, 11, 12, 13>;
-#endif
   // workspace position of tile bit k: passengers j2,j3,j5,j6 -> addr 0..3;
   // v bits (j0,j1,j7,j8,j9,j4,j10..13) -> addr 4..13 (P) or 14..23 (Q).
   using AOutP = ListMap<4, 5, 0, 1, 9, 2, 3, 6, 7, 8, 10, 11, 12, 13>;         // tile base a << 14
@@ -121,11 +97,7 @@ struct SweepF32M24 {
   using BL0 = Layout<BL<0, 1, 7, 8, 9, 10, 11>, BL<2, 3, 4, 5, 6, 12, 13>>;
   using BL1 = Layout<BL<13, 12, 4, 5, 6, 0, 1>, BL<11, 10, 9, 8, 7, 2, 3>>;
   using BS = Swz<9, 2, 10, 3, 11, 4>;
-#if CHW_SWEEP_REBAL
   using BB0 = BL<0, 1, 7, 8, 9, 10, 11>;
-#else
-  using BB0 = BL<7, 8, 9, 10, 11>;
-#endif
   using BB1 = BL<4, 5, 6, 12, 13>;
   // B tile positions in a layout-P workspace (tile base v << 4); layout Q: IdMap (base v << 14).
   using BInP = ListMap<0, 1, 2, 3, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23>;
@@ -238,32 +210,6 @@ __device__ __forceinline__ void smem_load_half(const float* sm, float (&w)[E2], 
     }
   });
 }
-// Registers of layout L -> shared memory at the positions of Map (vectorized
-// like store_global): used to stage a tile in its global order for a TMA store.
-template <class L, class Map, int E>
-__device__ __forceinline__ void smem_store_map(float* sm, const float (&v)[E], uint32_t tid) {
-  constexpr int VB = vec_bits<L, Map>(2);
-  const uint32_t tb = thr_off<L, Map>(tid);
-  static_for<L::E>([&](auto R) {
-    constexpr int r = decltype(R)::value;
-    if constexpr (vec_head<L, Map>(r, VB)) {
-      constexpr uint32_t ro = reg_off<L, Map>(r);
-      float tmp[1 << VB];
-      static_for<(1 << VB)>([&](auto Q) { tmp[decltype(Q)::value] = v[vec_elem<L, Map>(r, decltype(Q)::value, VB)]; });
-      SmemVec<float, VB>::st(sm + (tb + ro), tmp);
-    }
-  });
-}
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tensor4_s2g(const void* tmap, const void* ssrc, int x, int y, int z, int w) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(tmap),
-               "r"(smem_u32(ssrc)), "r"(x), "r"(y), "r"(z), "r"(w)
-               : "memory");
-}
 __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -314,12 +260,12 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
   constexpr int TILE = P::TILE;
   constexpr uint32_t TB = TILE * 4;
   constexpr int NT = P::NT;
-  constexpr int SA = CHW_SWEEP_BLDG ? 3 : 2;
+  constexpr int SA = 2;
   constexpr int MAXT = 8;  // tiles per CTA per row (ceil(1024 / 148) = 7)
   extern __shared__ __align__(128) float smem_sw[];
   float* ringA = smem_sw;
-  float* stageB = smem_sw + SA * TILE;  // (unused with CHW_SWEEP_BLDG)
-  float* bufB = CHW_SWEEP_BLDG ? stageB : stageB + TILE;  // TILE / 2 floats: the B transpose buffer
+  float* stageB = smem_sw + SA * TILE;
+  float* bufB = stageB + TILE;  // TILE / 2 floats: the B transpose buffer
   __shared__ __align__(8) uint64_t fullA[SA], fullB, regionfree[MAXT];
   const uint32_t tid = threadIdx.x;
   const uint32_t G = gridDim.x, c = blockIdx.x;
@@ -369,32 +315,6 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       smem_store<P::AL0, P::AS>(stage, v, gtv);
       bar();
       smem_load<P::AL1, P::AS>(stage, v, gtv);
-#if CHW_SWEEP_ATMA
-      butterflies<P::AL1, P::AB1, false>(v);
-      SWEEP_STAMP(0, 2);
-      if (r >= 1) mbar_wait_cta(&regionfree[i], (r - 1) & 1u);  // B(r-1, a) has been read
-      SWEEP_STAMP(0, 3);
-      bar();  // every thread has read the stage: stage the result in it (the
-              // region order: layout P's contiguous region = layout Q's box order)
-      smem_store_map<P::AL1, P::AOutP>(stage, v, gtv);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      bar();
-      if (gt == 0) {
-        const uint32_t a = tile_of(c + i * G);
-        if (r & 1u)
-          tensor4_s2g(&tmapP, stage, 0, (int)a, 0, 0);  // layout Q: 1024 runs of 64 B
-        else
-          bulk_s2g(ws + ((uint64_t)a << 14), stage, TB);  // layout P: contiguous 64 KiB
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        if (u + SA < total) issue(u + SA);  // the store has read the stage: refill it
-        if (i + 1 == nt) {  // this CTA's last A tile of row r: publish all nt of them
-          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          red_release_add(&cnt[r], nt);
-        }
-      }
-#else
       bar();  // every thread has read the stage: refill it
       if (gt == 0 && u + SA < total) {
         // order the group's generic-proxy reads of the stage before the TMA write
@@ -417,7 +337,6 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
         bar();
         if (gt == 0) red_release_add(&cnt[r], nt);
       }
-#endif
       SWEEP_STAMP(0, 4);
     }
   } else {  // ---- B group
@@ -434,64 +353,6 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
     uint64_t* fullBp = (CHW_SWEEP_ONLY == 3) ? &fullA[bg] : &fullB;
     const uint32_t barid = 2 + bg;
     auto bar = [barid] { named_bar(barid, NT); };
-#if CHW_SWEEP_BLDG
-    // Load B tile u (this thread's 128 values, layout BL0) from the L2-resident
-    // workspace.  The first tile of a row needs every A tile of that row: with
-    // wait = false the call returns false if they are not all counted yet, and
-    // the thread loads the tile at the top of the next iteration instead.
-    auto load = [&](uint32_t u, bool wait, uint32_t gtv) -> bool {
-      const uint32_t r = u / nt, i = u - r * nt;
-      if (i == 0) {
-        if (ld_acquire_gpu_u32(&cnt[r]) < P::NTILES) {
-          if (!wait) return false;
-          while (ld_relaxed_u32(&cnt[r]) < P::NTILES) __nanosleep(64);
-          (void)ld_acquire_gpu_u32(&cnt[r]);  // synchronizes with every A tile's release
-        }
-      }
-      const uint32_t t = tile_of(c + i * G);
-      if (r & 1u)
-        load_global<P::BL0, IdMap, Cache::kL2>(ws + ((uint64_t)t << 14), v, gtv);
-      else
-        load_global<P::BL0, P::BInP, Cache::kL2>(ws + ((uint64_t)t << 4), v, gtv);
-      return true;
-    };
-    bool pending = total > 0;  // tile u not loaded yet
-    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
-      uint32_t gtv = gt;
-#if CHW_SWEEP_OPAQUE
-      asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
-#endif
-      SWEEP_STAMP(1, 0);
-      if (pending) load(u, true, gtv);
-      SWEEP_STAMP(1, 1);
-      butterflies<P::BL0, P::BB0, false>(v);  // every loaded value consumed
-      SWEEP_STAMP(1, 2);
-      const uint32_t t = tile_of(c + i * G);
-      float* orow = out + ((uint64_t)r << 24);
-      const uint32_t outer = deposit<P::BOuter>(t);
-      using MapO = typename std::conditional<SEQ, SeqMap<P::BOutH, 24>, P::BOutH>::type;
-      float w[P::E / 2];
-      bar();  // previous tile's buffer reads are done
-      smem_store_half<P::BH0, P::BHS, P::BL0_T0, 0>(bufB, v, gtv);
-      bar();
-      // every thread's loads of B(r, t) have returned: A(r+1, t) may overwrite it
-      if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
-      smem_load_half<P::BH1, P::BHS>(bufB, w, gtv);
-      bar();
-      smem_store_half<P::BH0, P::BHS, P::BL0_T0, 1>(bufB, v, gtv);
-      // v is free: prefetch the next tile into it while this one finishes
-      pending = (u + 1 < total) ? !load(u + 1, false, gtv) : false;
-      SWEEP_STAMP(1, 4);
-      butterflies<P::BH1, P::BHB1, false>(w);
-      store_global<P::BH1, MapO, SCALE, Cache::kStream>(orow, w, gtv, scale, outer);
-      SWEEP_STAMP(1, 6);
-      bar();
-      smem_load_half<P::BH1, P::BHS>(bufB, w, gtv);
-      butterflies<P::BH1, P::BHB1, false>(w);
-      store_global<P::BH1, MapO, SCALE, Cache::kStream>(orow, w, gtv, scale, outer | (1u << 21));
-      SWEEP_STAMP(1, 3);
-    }
-#else
     uint64_t pol = 0;
     // Issue workspace tile u into the (free) B stage.  The first tile of a row
     // needs every A tile of that row: with wait = false the call returns
@@ -531,26 +392,10 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
 #endif
       mbar_wait_cta(fullBp, (u / ustep) & 1u);
       SWEEP_STAMP(1, 2);
-#if CHW_SWEEP_DISCARD
-      // Layout-Q tiles are whole 64 KiB regions: drop their now-dead L2 lines
-      // (no write-back) instead of letting them be evicted dirty before
-      // A(r+1, t) rewrites them — before `regionfree` lets A write there.
-      // (Layout-P tiles share every 128-byte line with another CTA's tile.)
-      if (r & 1u) {
-        const float* reg = ws + ((uint64_t)tile_of(c + i * G) << 14);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) discard_l2_128(reg + (gt + q * NT) * 32u);
-      }
-#else
       // B(r, t)'s workspace bytes are in shared memory: A(r+1, t) may overwrite them.
       if (gt == 0 && CHW_SWEEP_ONLY != 3) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
-#endif
       smem_load<P::BL0, NoSwz>(stageB, v, gtv);
       bar();  // the stage is read: load the next B tile while this one is computed
-#if CHW_SWEEP_DISCARD
-      // every thread's discards are done: A(r+1, t) may overwrite the region
-      if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
-#endif
       if (gt == 0 && u + ustep < total) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         pending = !issue(u + ustep, false);
@@ -580,7 +425,6 @@ __global__ void __launch_bounds__(2 * SweepF32M24::NT, 1)
       store_global<P::BH1, MapO, SCALE, Cache::kStream>(orow, w, gtv, scale, outer | (1u << 21));
       SWEEP_STAMP(1, 3);
     }
-#endif
   }
 }
 
@@ -713,195 +557,6 @@ __global__ void __launch_bounds__(2 * SweepNatF32M24::NT, 1)
       butterflies<P::BL1, P::BB1, false>(v);
       const uint32_t t = c + i * G;  // v bits = j4..j13 in order: natural position t << 4
       store_global<P::BL1, P::BOut, SCALE, Cache::kStream>(out + ((uint64_t)r << 24), v, gtv, scale, t << 4);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K9b: the same single-pass sweep with 64-value threads and 16 warps per SM
-// (4 per sub-partition instead of 2: the 128-value version was latency bound,
-// IPC ~0.15 per warp, tools/sweep_trace.py).  A tiles (64 KiB, 256 threads)
-// take three layouts (j0, j1 stay in registers throughout, so every shared
-// round trip is a 16-byte vector access); B tiles shrink to 32 KiB (3
-// passengers = 32-byte runs + j14..23, 128 threads, three layouts), two per
-// A tile, handled by two B groups with one 32 KiB stage each.
-//
-// Workspace (layout P, even rows): addr[0..2] = passengers (j0, j1, j5),
-// addr[3..13] = v (B tile index, 11 bits), addr[14..23] = a (j14..23).
-// Layout Q (odd rows): addr[0..2] passengers, addr[3..12] = a,
-// addr[13..23] = v.  A(r+1, a) overwrites exactly B(r, a), B(r, a + 1024)
-// (r even) or B(r, 2a), B(r, 2a + 1) (r odd): CTA c owns A tiles
-// a_i = c + i G and those B tiles; B group g takes the g-th of each pair.
-// ---------------------------------------------------------------------------
-struct SweepBF32M24 {
-  static constexpr int M = 24;
-  static constexpr int ATILE = 1 << 14, BTILE = 1 << 13;
-  static constexpr int NTA = 256, NTB = 128;
-  static constexpr uint32_t NTILES = 1024;  // A tiles per row (B tiles: 2048)
-  // A: tile bit k = j bit k.
-  using AL0 = Layout<BL<0, 1, 5, 6, 7, 8>, BL<2, 3, 4, 9, 10, 11, 12, 13>>;
-  using AL1 = Layout<BL<0, 1, 2, 3, 4, 9>, BL<5, 6, 7, 8, 10, 11, 12, 13>>;
-  using AL2 = Layout<BL<0, 1, 10, 11, 12, 13>, BL<5, 6, 7, 8, 9, 2, 3, 4>>;
-  using AS1 = Swz<5, 2, 6, 3, 7, 4>;
-  using AS2 = Swz<5, 2, 6, 3, 7, 4>;
-  using AB0 = BL<0, 1, 5, 6, 7, 8>;
-  using AB1 = BL<2, 3, 4, 9>;
-  using AB2 = BL<10, 11, 12, 13>;
-  // passengers j0, j1, j5 -> addr 0..2; v0..v10 = j6, j7, j8, j9, j2, j3, j4, j10..j13
-  using AOutP = ListMap<0, 1, 7, 8, 9, 2, 3, 4, 5, 6, 10, 11, 12, 13>;         // tile base a << 14
-  using AOutQ = ListMap<0, 1, 17, 18, 19, 2, 13, 14, 15, 16, 20, 21, 22, 23>;  // tile base a << 3
-  // B: t0..t2 = passengers (addr 0..2), t3..t12 = j14..j23.
-  using BL0 = Layout<BL<0, 1, 7, 8, 9, 10>, BL<2, 3, 4, 5, 6, 11, 12>>;
-  using BL1 = Layout<BL<0, 1, 3, 4, 5, 6>, BL<7, 8, 9, 10, 2, 11, 12>>;
-  using BL2 = Layout<BL<12, 11, 0, 1, 3, 4>, BL<10, 9, 8, 7, 2, 5, 6>>;
-  using BS1 = Swz<7, 2, 8, 3, 9, 4>;
-  using BS2 = Swz<7, 2, 10, 2, 8, 3, 9, 4>;
-  using BB0 = BL<7, 8, 9, 10>;
-  using BB1 = BL<3, 4, 5, 6>;
-  using BB2 = BL<11, 12>;
-  // dyadic output position (bit q = j bit 23 - q) of tile bit t and of v's bits
-  using BOut = ListMap<23, 22, 18, 9, 8, 7, 6, 5, 4, 3, 2, 1, 0>;
-  using BOuter = BL<17, 16, 15, 14, 21, 20, 19, 13, 12, 11, 10>;
-  static_assert(AL0::NT == NTA && BL0::NT == NTB && AL0::E == 64 && BL0::E == 64, "group shape");
-};
-
-template <bool SCALE>
-__global__ void __launch_bounds__(SweepBF32M24::NTA + 2 * SweepBF32M24::NTB, 1)
-    sweep_b_m24_kernel(const float* __restrict__ in, float* __restrict__ out, float* __restrict__ ws,
-                       uint32_t* __restrict__ cnt, uint32_t rows, float scale,
-                       const __grid_constant__ TmapParam tmapP) {
-  using P = SweepBF32M24;
-  constexpr uint32_t TBA = P::ATILE * 4, TBB = P::BTILE * 4;
-  constexpr int SA = 2;
-  constexpr int MAXT = 8;
-  extern __shared__ __align__(128) float smem_sb[];
-  float* ringA = smem_sb;
-  float* stB = smem_sb + SA * P::ATILE;  // two B stages, one per B group
-  __shared__ __align__(8) uint64_t fullA[SA], fullB[2], regionfree[MAXT];
-  const uint32_t tid = threadIdx.x;
-  const uint32_t G = gridDim.x, c = blockIdx.x;
-  const uint32_t nt = (P::NTILES - c + G - 1) / G;
-  if (nt == 0 || nt > MAXT) return;
-  if (tid == 0) {
-    for (int s = 0; s < SA; ++s) mbar_init_cta(&fullA[s], 1);
-    mbar_init_cta(&fullB[0], 1);
-    mbar_init_cta(&fullB[1], 1);
-    for (int k = 0; k < MAXT; ++k) mbar_init_cta(&regionfree[k], 2);  // both B groups
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const uint32_t total = rows * nt;
-  float v[64];
-  if (tid < (uint32_t)P::NTA) {  // ---- A group (8 warps)
-    const uint32_t gt = tid;
-    auto bar = [] { named_bar(1, P::NTA); };
-    uint64_t pol = 0;
-    auto issue = [&](uint32_t u) {
-      const uint32_t r = u / nt, i = u - r * nt;
-      const int st = (int)(u % SA);
-      mbar_expect_tx_cta(&fullA[st], TBA);
-      const uint64_t a = c + (uint64_t)i * G;
-      bulk_g2s(ringA + st * P::ATILE, in + ((uint64_t)r << 24) + (a << 14), TBA, &fullA[st], pol);
-    };
-    if (gt == 0) {
-      pol = l2_evict_first_policy();
-      for (uint32_t u = 0; u < (uint32_t)SA && u < total; ++u) issue(u);
-    }
-    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
-      const int st = (int)(u % SA);
-      float* stage = ringA + st * P::ATILE;
-      uint32_t gtv = gt;
-      asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
-      mbar_wait_cta(&fullA[st], (u / SA) & 1u);
-      smem_load<P::AL0, NoSwz>(stage, v, gtv);
-      butterflies<P::AL0, P::AB0, false>(v);
-      bar();
-      smem_store<P::AL0, P::AS1>(stage, v, gtv);
-      bar();
-      smem_load<P::AL1, P::AS1>(stage, v, gtv);
-      butterflies<P::AL1, P::AB1, false>(v);
-      bar();
-      smem_store<P::AL1, P::AS2>(stage, v, gtv);
-      bar();
-      smem_load<P::AL2, P::AS2>(stage, v, gtv);
-      bar();  // every thread has read the stage: refill it
-      if (gt == 0 && u + SA < total) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(u + SA);
-      }
-      butterflies<P::AL2, P::AB2, false>(v);
-      if (r >= 1) mbar_wait_cta(&regionfree[i], (r - 1) & 1u);  // both B(r-1, .) tiles read
-      const uint32_t a = c + i * G;
-      if (r & 1u)
-        store_global<P::AL2, P::AOutQ, false, Cache::kL2>(ws + ((uint64_t)a << 3), v, gtv, 1.0f);
-      else
-        store_global<P::AL2, P::AOutP, false, Cache::kL2>(ws + ((uint64_t)a << 14), v, gtv, 1.0f);
-      if (i + 1 == nt) {
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        bar();
-        if (gt == 0) red_release_add(&cnt[r], nt);
-      }
-    }
-  } else {  // ---- B groups (4 warps each)
-    const uint32_t g = (tid - P::NTA) / P::NTB;
-    const uint32_t gt = (tid - P::NTA) % P::NTB;
-    const uint32_t barid = 2 + g;
-    auto bar = [barid] { named_bar(barid, P::NTB); };
-    float* stage = stB + g * P::BTILE;
-    uint64_t pol = 0;
-    auto tile_of = [&](uint32_t r, uint32_t i) -> uint32_t {
-      const uint32_t a = c + i * G;
-      return (r & 1u) ? 2 * a + g : a + 1024 * g;
-    };
-    auto issue = [&](uint32_t u, bool wait) -> bool {
-      const uint32_t r = u / nt, i = u - r * nt;
-      if (i == 0) {
-        if (ld_relaxed_u32(&cnt[r]) < P::NTILES) {
-          if (!wait) return false;
-          while (ld_relaxed_u32(&cnt[r]) < P::NTILES) __nanosleep(64);
-        }
-        (void)ld_acquire_gpu_u32(&cnt[r]);
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-      }
-      mbar_expect_tx_cta(&fullB[g], TBB);
-      const uint32_t t = tile_of(r, i);
-      if (r & 1u)
-        bulk_g2s(stage, ws + ((uint64_t)t << 13), TBB, &fullB[g], pol);
-      else
-        tensor4_g2s_hint(stage, &tmapP, 0, (int)t, 0, 0, &fullB[g], pol);
-      return true;
-    };
-    bool pending = false;
-    if (gt == 0) {
-      pol = l2_evict_normal_policy();
-      pending = total > 0;
-    }
-    for (uint32_t u = 0, r = 0, i = 0; u < total; ++u, i = (i + 1 == nt) ? 0 : i + 1, r += (i == 0)) {
-      if (pending) pending = !issue(u, true);
-      uint32_t gtv = gt;
-      asm volatile("mov.b32 %0, %1;" : "=r"(gtv) : "r"(gt));
-      mbar_wait_cta(&fullB[g], u & 1u);
-      if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&regionfree[i])) : "memory");
-      smem_load<P::BL0, NoSwz>(stage, v, gtv);
-      butterflies<P::BL0, P::BB0, false>(v);
-      bar();
-      smem_store<P::BL0, P::BS1>(stage, v, gtv);
-      bar();
-      smem_load<P::BL1, P::BS1>(stage, v, gtv);
-      butterflies<P::BL1, P::BB1, false>(v);
-      bar();
-      smem_store<P::BL1, P::BS2>(stage, v, gtv);
-      bar();
-      smem_load<P::BL2, P::BS2>(stage, v, gtv);
-      bar();  // the stage is free: load this group's next B tile
-      if (gt == 0 && u + 1 < total) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        pending = !issue(u + 1, false);
-      }
-      butterflies<P::BL2, P::BB2, false>(v);
-      const uint32_t t = tile_of(r, i);
-      store_global<P::BL2, P::BOut, SCALE, Cache::kStream>(out + ((uint64_t)r << 24) + deposit<P::BOuter>(t), v,
-                                                            gtv, scale);
     }
   }
 }

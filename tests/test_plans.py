@@ -1,6 +1,7 @@
 """CPU checks of the round-2 tile plans with the offline cost model
-(tools/plan_check.py): every shared-memory round trip of the K9 / K9b row
-sweeps is bank-conflict free (wavefronts == ideal), every global access moves
+(tools/plan_check.py): every shared-memory round trip of the K9 row sweep
+(dyadic and natural-order plans) and of the K10 cluster kernel is
+bank-conflict free (wavefronts == ideal), every global access moves
 whole 32-byte sectors, and every butterfly bit is covered exactly once."""
 import os
 import sys
@@ -56,18 +57,33 @@ def test_k9_butterfly_coverage():
     assert a_bits | b_bits == set(range(24))
 
 
-def test_k9b_layouts_conflict_free():
-    a0 = Layout([0, 1, 5, 6, 7, 8], [2, 3, 4, 9, 10, 11, 12, 13])
-    a1 = Layout([0, 1, 2, 3, 4, 9], [5, 6, 7, 8, 10, 11, 12, 13])
-    a2 = Layout([0, 1, 10, 11, 12, 13], [5, 6, 7, 8, 9, 2, 3, 4])
-    s = [(5, 2), (6, 3), (7, 4)]
-    for c in (smem_cost(a0, [], 4, 2), smem_cost(a0, s, 4, 2), smem_cost(a1, s, 4, 2),
-              smem_cost(a2, s, 4, 2)):
-        assert _ideal(c)
-    b1 = Layout([0, 1, 3, 4, 5, 6], [7, 8, 9, 10, 2, 11, 12])
-    b2 = Layout([12, 11, 0, 1, 3, 4], [10, 9, 8, 7, 2, 5, 6])
-    s2 = [(7, 2), (10, 2), (8, 3), (9, 4)]
-    assert _ideal(smem_cost(b1, s2, 4, 2)) and _ideal(smem_cost(b2, s2, 4, 2))
+def test_k9n_natural_plan():
+    """K9n (csrc/sweep.cuh: SweepNatF32M24): natural order folded into the
+    sweep — 16-byte accesses on both sides of A's transpose, B's first layout
+    conflict-free under TMA's 64-byte swizzle, in-place transpose, scalar
+    stores in whole sectors; every row bit butterflied exactly once."""
+    a0 = Layout([0, 1, 5, 6, 7, 8, 9], [2, 3, 4, 10, 11, 12, 13])
+    a1 = Layout([0, 1, 4, 10, 11, 12, 13], [2, 3, 5, 6, 7, 8, 9])
+    a_s = [(5, 4)]
+    for c in (smem_cost(a0, [], 4, 2, 4), smem_cost(a0, a_s, 4, 2, 4), smem_cost(a1, a_s, 4, 2, 4)):
+        assert _ideal(c) and c[2] == 2          # all three are 16-byte vector accesses
+    out_p = list(range(14))
+    out_q = [0, 1, 2, 3] + list(range(14, 24))
+    for pos in (out_p, out_q):
+        g = global_cost(a1, lambda b: pos[b], 4, 2, 4)
+        assert g["vec_bytes"] == 16 and g["partial_sectors_per_instr"] == 0
+    b0 = Layout([0, 1, 2, 3, 7, 8, 9], [4, 5, 6, 10, 11, 12, 13])
+    b1 = Layout([4, 5, 6, 10, 11, 12, 13], [0, 1, 2, 3, 7, 8, 9])
+    tma64 = [(5, 2), (6, 3)]                    # CU_TENSOR_MAP_SWIZZLE_64B on float-index bits
+    bs = [(5, 2), (6, 3), (7, 4)]
+    assert _ideal(smem_cost(b0, tma64, 4, 2, 4))
+    assert _ideal(smem_cost(b0, bs, 4, 2, 4)) and _ideal(smem_cost(b1, bs, 4, 2, 4))
+    g = global_cost(b1, lambda b: out_q[b], 4, 2, 4)   # natural position of B tile bit t
+    assert g["partial_sectors_per_instr"] == 0 and g["sectors_per_instr"] == 4
+    a_bits = {0, 1, 5, 6, 7, 8, 9} | {4, 10, 11, 12, 13}
+    t_to_j = {0: 0, 1: 1, 2: 2, 3: 3, **{k: 10 + k for k in range(4, 14)}}
+    b_bits = {t_to_j[t] for t in ({2, 3, 7, 8, 9} | {4, 5, 6, 10, 11, 12, 13})}
+    assert a_bits.isdisjoint(b_bits) and a_bits | b_bits == set(range(24))
 
 
 def test_k10_cluster_plan():
