@@ -96,14 +96,27 @@ __device__ __forceinline__ void mbar_expect_tx_cta(uint64_t* bar, uint32_t bytes
                "r"(bytes)
                : "memory");
 }
+#ifndef CHW_MBAR_HINT
+#define CHW_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait_cta(uint64_t* bar, uint32_t parity) {
   uint32_t ok = 0;
   while (!ok) {
+#if CHW_MBAR_HINT
+    // suspend-time hint (ns): the warp sleeps in hardware until the phase
+    // completes instead of re-polling every few hundred cycles
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"((uint32_t)CHW_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+#endif
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
