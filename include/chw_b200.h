@@ -95,8 +95,11 @@ chw_status chw_b200_forward_ordered(const void* in, void* out, chw_dtype dtype, 
                                     size_t workspace_bytes, void* stream);
 
 /* Workspace the device call needs (0 for single-pass sizes), and for a call
- * with an explicit order (NATURAL/SEQUENCY add one batch-sized buffer: the
- * dyadic result is gathered into the requested order in one coalesced pass). */
+ * with an explicit order.  NATURAL and SEQUENCY are folded into the kernels'
+ * stores — no extra workspace — for every single-pass size and for f32 rows
+ * of 2^16 and 2^24; for the other long rows they add one batch-sized buffer
+ * (the dyadic result is gathered into the requested order in one coalesced
+ * pass). */
 size_t chw_b200_workspace_bytes(chw_dtype dtype, int64_t batch, uint64_t n);
 size_t chw_b200_workspace_bytes_ordered(chw_dtype dtype, int64_t batch, uint64_t n, chw_order order);
 
