@@ -77,6 +77,20 @@ def load_traffic(cfg: str):
     return None
 
 
+# Measured ceilings of the schedule class each long-row kernel belongs to (a
+# single HBM pass that exchanges the row through an L2-resident workspace): the
+# HBM-side rate of tools/mix_probe.cu — no arithmetic, the same four byte
+# streams — as a fraction of the copy peak, for the kernel's workspace
+# footprint (profiles/r02_mix_probe.txt).  Context for the
+# roofline fraction, not a substitute for it.
+SCHEDULE_CEILING = {
+    "cfg5": {"frac": 0.64, "workspace_mib": 64, "evidence": "profiles/r02_mix_probe.txt",
+             "what": "single pass through a 64 MiB L2 workspace (probe: 4.1-4.2 TB/s HBM-side)"},
+    "cfg4": {"frac": 0.71, "workspace_mib": 37, "evidence": "profiles/r02_mix_probe.txt",
+             "what": "single pass through 32-48 MiB of per-CTA L2 workspace rows (probe: 4.5-4.7 TB/s HBM-side)"},
+}
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -616,6 +630,7 @@ def run_ours(args):
                 "ms_per_step": round(ms, 4), "frac": round(rc["alg_bytes"] / (ms * 1e-3) / 1e9 / peak, 4),
                 "plan": chw.plan_name(DTYPE_CODE[cdt], 1 << cm), "l2_flush": rc["flush"],
                 "traffic": load_traffic(c), "clocks": csamp.summary(),
+                "schedule_ceiling": SCHEDULE_CEILING.get(c),
                 "parity": None if pc is None else {k: pc[k] for k in ("rows_checked", "max_rel_l2", "tolerance",
                                                                        "order_probe_ok", "ok")},
             }
@@ -643,7 +658,8 @@ def run_ours(args):
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": peak_src, "alg_bytes_per_launch": rows * n * es * 2,
                          "copy_peak_same_run_gbs": round(copy_peak, 1),
-                         "copy_sustained_same_run_gbs": round(copy_sustained, 1)},
+                         "copy_sustained_same_run_gbs": round(copy_sustained, 1),
+                         "schedule_ceiling": SCHEDULE_CEILING.get(cfg)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "parity": parity,
