@@ -6,13 +6,18 @@
 // whole chip on one row at a time, both phases concurrently:
 //
 //   A(r, a): contiguous 64 KiB input tile a (j bits 14..23 = a) of row r,
-//            TMA bulk copy into a 2-stage ring -> butterflies on j bits 0..13
-//            (7 register bits, one in-place smem transpose, 7 more) -> the
-//            row workspace W (L2-resident, ld/st .cg);
-//   B(r, v): B tile v of W (4 "passenger" j bits kept together for 64-byte
-//            runs + j bits 14..23), one TMA copy from L2 ->
-//            butterflies on j bits 14..23 -> dyadic output (16-byte stores,
-//            512 contiguous bytes per warp instruction).
+//            TMA bulk copy into a 2-stage ring -> butterflies on j bits 0, 1
+//            and 4..13 (7 register bits, one in-place smem transpose, 5 more)
+//            -> the row workspace W (L2-resident, st .cg);
+//   B(r, v): B tile v of W (4 "passenger" j bits 2, 3, 5, 6 kept together for
+//            64-byte runs + j bits 14..23), one TMA copy from L2 ->
+//            butterflies on j bits 2, 3 and 14..23 (7 register bits, the
+//            transpose through a 32 KiB buffer one half at a time, 5 more) ->
+//            dyadic output (16-byte stores, 512 contiguous bytes per warp
+//            instruction).
+// The NATURAL-order plan of the same sweep (K9n, SweepNatF32M24 /
+// sweep_nat_m24_kernel) is further down; what bounds both — the SM<->L2 fabric,
+// not the SM side — is measured in DESIGN.md §4.1a.
 //
 // Workspace layouts alternate per row (P for even rows, Q for odd):
 //   P: addr[0..3] = passengers, addr[4..13] = v bits, addr[14..23] = a bits;
@@ -26,8 +31,9 @@
 // (cooperative launch, one CTA per SM), so the waits cannot deadlock.
 //
 // Roles per CTA (256 threads): warps 0-3 A group, warps 4-7 B group; thread
-// 0 of each group issues its TMA copies.  Shared memory: 2 A stages + 1 B
-// stage (64 KiB each, tiles transposed in place).
+// 0 of each group issues its TMA copies.  Shared memory: 2 A stages (tiles
+// transposed in place) + 1 B stage (64 KiB each) + the 32 KiB B transpose
+// buffer.
 //
 // Every layout/swizzle/position map below was checked with tools/plan_check.py
 // (tools/swz_search.py): all shared-memory accesses conflict-free, every
