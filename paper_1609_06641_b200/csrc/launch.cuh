@@ -19,7 +19,6 @@
 #include "pipelined.cuh"
 #include "rowpipe.cuh"
 #include "clusterm16.cuh"
-#include "rowpipe3.cuh"
 #include "k1t.cuh"
 #include "passtma.cuh"
 
@@ -389,33 +388,16 @@ chw_status launch_rowpipe_m16(const float* in, float* out, void* ws, int64_t bat
 // f32 m = 16 schedule: 'c' K10 cluster/DSMEM kernel (clusterm16.cuh), 'r' K6
 // row pipeline (default).  K11, the row pipeline with 128-value threads (half
 // the instructions, four shared-memory passes), measured +3 % under the soak
-// and -13 % cold against K6 and was removed (profiles/r02_ab_k11.txt).
+// and -13 % cold against K6 and was removed; so was K12, the same idea with
+// four groups of 64-value threads and a 6 + 10 level split (+3.4 % soaked,
+// -3..-10 % cold) (profiles/r02_ab_k11.txt).
 inline char m16_mode() {
   static const char mode = [] {
     const char* e = std::getenv("CHW_B200_M16");
-    return (e && (e[0] == 'c' || e[0] == 'q')) ? e[0] : 'r';
+    return (e && e[0] == 'c') ? 'c' : 'r';
   }();
   return mode;
 }
-// K12 (rowpipe3.cuh): the row pipeline with a one-layout first phase; the same
-// per-CTA workspace rows as K6 (rowpipe_workspace).
-template <bool SCALE>
-chw_status launch_rowpipe3_m16(const float* in, float* out, void* ws, int64_t batch, float scale,
-                               cudaStream_t st) {
-  using P = RowPipe3F32M16;
-  constexpr auto k = rowpipe3_m16_kernel<SCALE>;
-  if (((uintptr_t)in | (uintptr_t)out | (uintptr_t)ws) & 15u)
-    return fail(CHW_ERR_ARGUMENT, "chw_forward: buffers and workspace must be 16-byte aligned");
-  constexpr int smem = 6 * P::TILE * 4;  // one stage per A group, two per B group
-  if (chw_status s = prep_kernel<k>(smem)) return s;
-  int dev = 0, sms = 0;
-  if (chw_status s = current_device(&dev)) return s;
-  CHW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const unsigned grid = (unsigned)std::min<int64_t>(batch, (int64_t)sms);
-  k<<<grid, 4 * P::NT, smem, st>>>(in, out, static_cast<float*>(ws), (uint64_t)batch, scale);
-  return check_launch("rowpipe3_m16_kernel");
-}
-
 // K10: clusters of 4 CTAs, one row per cluster at a time, no workspace.
 template <bool SCALE>
 chw_status launch_cluster_m16(const float* in, float* out, int64_t batch, float scale, cudaStream_t st) {
@@ -565,7 +547,6 @@ chw_status launch_m(const T* in, T* out, void* ws, int64_t batch, typename IoTra
     return launch_k1<T, M, SC>(in, out, batch, scale, st);
   } else if constexpr (std::is_same<T, float>::value && M == 16) {
     if (m16_mode() == 'c') return launch_cluster_m16<SC == Scaling::kDeferred>(in, out, batch, scale, st);
-    if (m16_mode() == 'q') return launch_rowpipe3_m16<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
     return launch_rowpipe_m16<SC == Scaling::kDeferred>(in, out, ws, batch, scale, st);
   } else if constexpr (std::is_same<T, float>::value && M == 24) {
     if (m24_mode() == 's') return launch_sweep_m24(SC == Scaling::kDeferred, in, out, ws, batch, scale, st);
@@ -598,7 +579,7 @@ const char* plan_name_m(int m) {
         if (tc_bf16_m7_enabled()) return "k7tc-tcgen05";
       return K1Select<T, M>::kTuned ? "k1-tuned" : "k1-generic";
     } else if constexpr (std::is_same<T, float>::value && M == 16) {
-      return m16_mode() == 'c' ? "k10-cluster-dsmem" : m16_mode() == 'q' ? "k12-rowpipe-6-10" : "k6-rowpipe";
+      return m16_mode() == 'c' ? "k10-cluster-dsmem" : "k6-rowpipe";
     } else if constexpr (std::is_same<T, float>::value && M == 24) {
       return m24_mode() == 's' ? "k9-row-sweep" : "k4t-two-pass-tma";
     } else {
